@@ -1,0 +1,185 @@
+/*
+ * nbx.h -- C ABI of the B200-native nanoBragg spot simulator.
+ *
+ * This is the drop-in boundary for the reference's spot path
+ * (xtrace.kernels.nanobragg_spots, /root/reference/pkg/src/xtrace/kernels.py:219-276).
+ * The Python host layer (paper_2205_07976_b200/_native.py) binds it with
+ * ctypes, which releases the GIL for the duration of every call.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, doubles.  No torch, no C++ types.
+ *   - Every array in a descriptor is caller-owned HOST memory, read (and for
+ *     the plan API copied to the device) during the call; nothing is retained.
+ *   - Output buffers are caller-owned; `out_on_device` says whether `out` is a
+ *     device pointer (on the context's device) or a host pointer.
+ *   - Nothing throws across the ABI.  Every entry point returns an NBX_* status;
+ *     the message of the last failure is nbx_last_error(ctx).
+ *   - One context per GPU; a context (and the plans made from it) must be used
+ *     from one host thread at a time.
+ *
+ * Reference interfaces each entry point replaces are cited per function.
+ */
+#ifndef NBX_H
+#define NBX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NBX_VERSION 10000 /* 1.0.0 */
+
+/* Status codes.  NBX_ERR_ARG mirrors ShapeMismatchError / ValueError
+ * (kernels.py:204-208), NBX_ERR_NUMERICAL mirrors NumericalFault wrapped in
+ * PatternFault (kernels.py:211-216, execution.py:183-185). */
+enum {
+    NBX_OK = 0,
+    NBX_ERR_ARG = 1,
+    NBX_ERR_NUMERICAL = 2,
+    NBX_ERR_CUDA = 3
+};
+
+/* Arithmetic path of the per-step evaluation. */
+enum {
+    NBX_COMPUTE_FP64 = 0, /* FP64 everywhere; parity 1e-9 vs the reference's FP64 math */
+    NBX_COMPUTE_FP32 = 1  /* FP64 geometry + FP64-exact phase split, FP32 sin/ratio; parity 1e-4 */
+};
+
+/* Output modes (what the fused epilogue writes per pixel). */
+enum {
+    NBX_OUT_F32 = 0,     /* out[p] = f32(scale*acc); the reference store (kernels.py:271-273) */
+    NBX_OUT_F64 = 1,     /* out[p] = scale*acc in f64 (extension; the reference rejects f64) */
+    NBX_OUT_ADD_F64 = 2, /* out[p] += f64(f32(scale*acc)): spots fused with add_array
+                            (kernels.py:315-331, scheduler.py:169-174) */
+    NBX_OUT_RAW_F64 = 3  /* out[p] += acc (unscaled FP64 partial, for channel shards) */
+};
+
+/* Lattice shape transforms.  SINCG is the reference's grating
+ * (kernels.py:115-142); the others follow the public nanoBragg definitions. */
+enum {
+    NBX_SHAPE_SINCG = 0,
+    NBX_SHAPE_GAUSS = 1,
+    NBX_SHAPE_ROUND = 2,
+    NBX_SHAPE_TOPHAT = 3
+};
+
+/* One rectangular pixel grid -- xtrace.model.DetectorPanel (model.py:328-371)
+ * plus the detector-thickness extension. */
+typedef struct nbx_panel {
+    int32_t slow_pixels;
+    int32_t fast_pixels;
+    int32_t thick_steps;         /* >= 1; 1 with thickness == 0 reproduces the reference */
+    int32_t reserved0;
+    double pixel_size;           /* m */
+    double distance;             /* m, sample to panel along the beam */
+    double beam_center[2];       /* (slow, fast) pixel coordinate of the direct beam */
+    double fast_axis[3];         /* unit */
+    double slow_axis[3];         /* unit, orthogonal to fast_axis */
+    double thickness;            /* m; 0 = infinitely thin sensor (reference semantics) */
+    double attenuation_length;   /* m; sensor absorption length (used when thickness > 0) */
+} nbx_panel;
+
+/* Everything one spot image needs -- the flattened SpotsContext
+ * (kernels.py:100-112) with CrystalModel (model.py:301-325),
+ * BeamSpectrum (model.py:374-406) and the panels. */
+typedef struct nbx_spots_desc {
+    /* detector */
+    int32_t n_panels;
+    int32_t oversample;          /* sub-pixel grid edge, >= 1 (kernels.py:169) */
+    const nbx_panel* panels;     /* n_panels; output is the panels' pixels concatenated */
+    /* beam */
+    double beam_direction[3];    /* unit */
+    int32_t polarization_on;
+    int32_t n_sources;
+    const double* wavelengths;   /* n_sources, Angstrom, > 0 */
+    const double* weights;       /* n_sources, >= 0 */
+    double fluence;              /* photons / m^2 */
+    double r_e_sqr;              /* m^2 */
+    /* crystal */
+    int32_t n_domains;           /* mosaic domains x phi steps */
+    int32_t shape;               /* NBX_SHAPE_* */
+    const double* bases;         /* n_domains x 3 x 3, rows a,b,c (Angstrom), already
+                                    rotated: CrystalModel.rotated_real_bases (model.py:317-325) */
+    int32_t n_cells[3];          /* Na, Nb, Nc >= 1 */
+    int32_t n_entries;
+    const int32_t* hkl;          /* n_entries x 3 Miller triples */
+    const double* amplitudes;    /* n_entries, finite, >= 0 */
+    double default_f;            /* amplitude of absent triples (model.py:264-279) */
+    /* normalisation: <= 0 means sum(weights) * n_domains * oversample^2
+     * (kernels.py:243-245); shards pass the GLOBAL value. */
+    double norm;
+    /* channel shard: evaluate sources [src_begin, src_end); src_end <= 0 -> all */
+    int32_t src_begin;
+    int32_t src_end;
+} nbx_spots_desc;
+
+/* Filled by nbx_plan_info. */
+typedef struct nbx_plan_info_t {
+    int64_t n_pixels;            /* output elements */
+    int64_t steps;               /* pixel x subpixel x thickness x source x domain */
+    int64_t table_cells;         /* dense Fhkl grid cells resident in HBM */
+    int32_t table_lo[3];         /* grid origin (h, k, l) */
+    int32_t table_dim[3];        /* grid extent */
+    int32_t compute;             /* NBX_COMPUTE_* */
+    int32_t table_kind;          /* 0 dense grid (magic index), 1 dense grid (wide index) */
+    double scale;                /* r_e^2 * fluence / norm */
+} nbx_plan_info_t;
+
+int nbx_version(void);
+
+/* Per-device context: stream, scratch, last error.  NULL on failure (no GPU). */
+void* nbx_ctx_create(int device);
+void nbx_ctx_destroy(void* ctx);
+const char* nbx_last_error(void* ctx);
+/* Launch on a caller stream (cudaStream_t as void*); NULL restores the ctx stream. */
+int nbx_ctx_set_stream(void* ctx, void* stream);
+int nbx_ctx_synchronize(void* ctx);
+
+/* Output elements a descriptor produces (sum of panel pixels); -1 if invalid. */
+int64_t nbx_output_pixels(const nbx_spots_desc* d);
+
+/* One-shot spot image: replaces nanobragg_spots(ctx, out) (kernels.py:219-276).
+ * first_bad (may be NULL) receives the lowest non-finite pixel or -1; on a
+ * fault the status is NBX_ERR_NUMERICAL and the output is unspecified, as in
+ * the reference (execution.py:217-224). */
+int nbx_spots(void* ctx, const nbx_spots_desc* d, int compute, int out_mode,
+              void* out, int out_on_device, int64_t* first_bad);
+
+/* Batch of independent images (SURVEY §8 E1 image sharding, config C3):
+ * outs[i] receives image i; images share nothing and launch back to back
+ * with device-to-host copies overlapped on a second stream. */
+int nbx_spots_batch(void* ctx, const nbx_spots_desc* descs, int n_images, int compute,
+                    int out_mode, void* const* outs, int out_on_device, int64_t* first_bad);
+
+/* Plan API: upload a descriptor once (tables, bases, channels resident in
+ * HBM), then run it any number of times. */
+void* nbx_plan_create(void* ctx, const nbx_spots_desc* d, int compute);
+int nbx_plan_run(void* plan, int out_mode, void* out, int out_on_device, int64_t* first_bad);
+int nbx_plan_info(void* plan, nbx_plan_info_t* info);
+/* Device-time of the last nbx_plan_run spot kernel (ms, CUDA events). */
+double nbx_plan_last_kernel_ms(void* plan);
+void nbx_plan_destroy(void* plan);
+
+/* Scale + store a reduced raw FP64 image (root of a channel-sharded image,
+ * SURVEY §8 E1): out = mode(scale * raw).  raw is a device pointer. */
+int nbx_finalize(void* ctx, const double* raw, int64_t n, double scale, int out_mode,
+                 void* out, int out_on_device, int64_t* first_bad);
+
+/* lhs[j] += (double) rhs[j] -- add_array (kernels.py:315-331). */
+int nbx_add_array(void* ctx, double* lhs, const float* rhs, int64_t n, int on_device);
+
+/* Poisson photon noise, bit-exact with the host twin nbx_poisson_host
+ * (SURVEY §8 X4): out[p] = Poisson(mean[p]) drawn from Philox4x32-10 keyed by
+ * (seed, image), counter = p.  mean/out are f64/f32 per `dtype` (0 f32, 1 f64). */
+int nbx_add_noise(void* ctx, const void* mean, void* out, int64_t n, int dtype,
+                  uint64_t seed, uint64_t image, int on_device);
+/* CPU twin of the same sampler (identical bits). */
+int nbx_poisson_host(const void* mean, void* out, int64_t n, int dtype,
+                     uint64_t seed, uint64_t image);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NBX_H */

@@ -1,0 +1,166 @@
+// nbx_device.cuh -- per-step device math of the spot kernel (sm_100a).
+//
+// Restates, for the GPU, the loop body of the reference spot kernel
+// (/root/reference/pkg/src/xtrace/kernels.py:247-273):
+//     h = (rel . a_m) / lambda_w                       kernels.py:253-260
+//     F_latt = sincg(pi h, Na) sincg(pi k, Nb) sincg(pi l, Nc)   kernels.py:134-142,261-263
+//     F_cell = table[round_half_away(h, k, l)]         kernels.py:145-146,264-268; model.py:264-279
+//     acc   += w * (F_cell * F_latt)^2                  kernels.py:269-270
+// Design notes:
+//   * sin(pi x) is evaluated on the REDUCED argument t = h - n (|t| <= 1/2) and
+//     r = N t - rint(N t), so no trigonometric range reduction is ever needed and
+//     the grating ratio sin(N pi t)/sin(pi t) becomes (r Q(r^2)) / (t Q(t^2)) with
+//     Q(s) = sin(pi sqrt s)/(pi sqrt s) a short even polynomial.  Only |F_latt|^2
+//     enters the image, so all signs (-1)^n, (-1)^k drop out.
+//   * The reference's limit branch (|sin x| < 1e-12 -> N cos(Nx)/cos(x)) is the
+//     t -> 0 limit of the same ratio; biasing |t| by a tiny constant makes the
+//     ratio evaluate to N there with no branch.
+//   * FP32 path: the fractional Miller index is split exactly (double-float
+//     product with FMA), so t carries ~3e-8 absolute error even for |h| ~ 50;
+//     the sin polynomials and the ratio then run in FP32.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nbx {
+
+// ---------------------------------------------------------------------------
+// Q(s) = sin(pi sqrt(s)) / (pi sqrt(s)), s in [0, 0.2704] (|x| <= 0.52).
+// Relative-minimax fits made by tools/fit_sinpi.py (mpmath, 60 digits).
+// FP32: degree 4, max rel err 9.1e-9.  FP64: degree 7, max rel err 2.9e-16.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float q_sinpi_f32(float s) {
+    float q = 0.02460929274903431744f;
+    q = __fmaf_rn(q, s, -0.1903951449679496331f);
+    q = __fmaf_rn(q, s, 0.8117093632737977162f);
+    q = __fmaf_rn(q, s, -1.644933097370079417f);
+    q = __fmaf_rn(q, s, 1.0f);
+    return q;
+}
+
+__device__ __forceinline__ double q_sinpi_f64(double s) {
+    double q = -0.000006705758238410946132099385;
+    q = __fma_rn(q, s, 0.000148310321408001520683082);
+    q = __fma_rn(q, s, -0.002346053946710248122556649);
+    q = __fma_rn(q, s, 0.02614784439741657402822952);
+    q = __fma_rn(q, s, -0.1907518238899222190335658);
+    q = __fma_rn(q, s, 0.8117424252758336467922741);
+    q = __fma_rn(q, s, -1.644934066848143329530488);
+    q = __fma_rn(q, s, 1.0);
+    return q;
+}
+
+__device__ __forceinline__ float rcp_approx_f32(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ double rcp_f64(double x) {
+    // MUFU seed + two Newton steps: full double precision for normal x.
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    return y;
+}
+
+// Round half away from zero, exactly as the reference evaluates it:
+// floor(x + 0.5) for x >= 0, ceil(x - 0.5) otherwise (kernels.py:145-146).
+// trunc(x + copysign(0.5, x)) is the same function bit for bit, including the
+// FP rounding of x +- 0.5.
+__device__ __forceinline__ double round_half_away(double x) {
+    return trunc(x + copysign(0.5, x));
+}
+
+// Bias added to |t| so that the grating ratio is finite at exact Bragg
+// positions (the reference's limit branch).  Chosen so that the product of
+// three biased terms stays a normal number in the path's precision.
+constexpr float kTBiasF32 = 1e-12f;
+constexpr double kTBiasF64 = 1e-30;
+
+// One axis of the FP64 grating: returns numerator r*Q(r^2) and denominator
+// t*Q(t^2) of |sin(N pi h)/sin(pi h)|, plus the rounded index and t.
+struct AxisF64 {
+    double num, den, n, t;
+};
+
+__device__ __forceinline__ AxisF64 axis_f64(double S, double iv, double N) {
+    AxisF64 a;
+    const double h = S * iv;                      // kernels.py:257-260 (sa * (1/lambda))
+    a.n = round_half_away(h);                     // lookup index, reference rounding
+    a.t = h - a.n;                                // exact (Sterbenz)
+    const double ta = fabs(a.t) + kTBiasF64;
+    const double k = rint(N * ta);
+    const double r = __fma_rn(N, ta, -k);         // N t - k, one rounding
+    a.num = r * q_sinpi_f64(r * r);
+    a.den = ta * q_sinpi_f64(ta * ta);
+    return a;
+}
+
+struct AxisF32 {
+    float num, den, n, t;
+};
+
+// S = S_hi + S_lo and 1/lambda = iv_hi + iv_lo are double-float splits of the
+// FP64 values; t = S*iv - rint(S*iv) is formed with one rounding at |t| <= 1/2
+// scale (the FMA absorbs the exact product error), so the phase is FP64-grade.
+__device__ __forceinline__ AxisF32 axis_f32(float S_hi, float S_lo, float iv_hi, float iv_lo,
+                                            float N) {
+    AxisF32 a;
+    const float p = S_hi * iv_hi;
+    a.n = rintf(p);
+    float t = __fmaf_rn(S_hi, iv_hi, -a.n);       // (S_hi*iv_hi - n) exactly, rounded once
+    t = __fmaf_rn(S_hi, iv_lo, t);
+    t = __fmaf_rn(S_lo, iv_hi, t);
+    a.t = t;
+    const float ta = fabsf(t) + kTBiasF32;
+    const float k = rintf(N * ta);
+    const float r = __fmaf_rn(N, ta, -k);
+    a.num = r * q_sinpi_f32(r * r);
+    a.den = ta * q_sinpi_f32(ta * ta);
+    return a;
+}
+
+// ---------------------------------------------------------------------------
+// Non-grating shape transforms, public nanoBragg definitions
+// with h0 = round_half_away(h) and fudge = 1:
+//   hrad^2 = sum_axes (N t)^2
+//   GAUSS : F_latt = NaNbNc exp(-hrad^2 / 0.63)
+//   ROUND : F_latt = NaNbNc 0.723601254558268 sinc3(pi sqrt(hrad^2)),
+//           sinc3(x) = 3 (sin x / x - cos x) / x^2
+//   TOPHAT: F_latt = NaNbNc if hrad^2 < 0.3969 else 0
+// Returned as F_latt^2.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T sinc3(T x) {
+    if (x < T(1e-4)) {
+        // series 1 - x^2/10 avoids the 0/0 cancellation
+        return T(1) - x * x * T(0.1);
+    }
+    T s, c;
+    if constexpr (sizeof(T) == 8) {
+        sincos(x, &s, &c);
+    } else {
+        sincosf(x, &s, &c);
+    }
+    return T(3) * (s / x - c) / (x * x);
+}
+
+template <int SHAPE, typename T>
+__device__ __forceinline__ T shape_latt2(T hrad2, T nnn) {
+    if constexpr (SHAPE == 1) {  // GAUSS
+        const T f = nnn * exp(-hrad2 / T(0.63));
+        return f * f;
+    } else if constexpr (SHAPE == 2) {  // ROUND
+        const T f = nnn * T(0.723601254558268) * sinc3<T>(T(3.14159265358979323846) * sqrt(hrad2));
+        return f * f;
+    } else {  // TOPHAT
+        return hrad2 < T(0.3969) ? nnn * nnn : T(0);
+    }
+}
+
+}  // namespace nbx

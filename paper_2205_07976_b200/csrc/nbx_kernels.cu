@@ -1,0 +1,325 @@
+// nbx_kernels.cu -- the spot kernel and its epilogue kernels (sm_100a).
+//
+// One thread owns one detector pixel (the reference's per-pixel contract,
+// kernels.py:1-7).  A 32x8 thread block covers 32 consecutive fast pixels in
+// each of 8 rows, so a warp's Fhkl gathers hit the same few L1 lines.  The
+// sub-pixel x thickness x domain x channel loops run in registers; the channel
+// table (1/lambda, weight) is staged once per block in shared memory and read
+// with one 16-byte LDS per step; rotated bases are warp-uniform __ldg loads
+// amortised over the channel loop.  Per-pixel accumulation is strictly
+// sequential, so the image is bitwise independent of launch geometry and
+// block order (test_kernels.py:208-246 contract).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "nbx_device.cuh"
+#include "nbx_kernels.cuh"
+#include "nbx_poisson.h"
+
+namespace nbx {
+
+enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3 };
+
+constexpr int kBlockX = 32;
+constexpr int kBlockY = 8;
+constexpr int kChanChunk = 64;  // FP32 partial sums are flushed to FP64 every 64 channels
+
+// ---------------------------------------------------------------------------
+// Sum over channels of w * F^2 * F_latt^2 for one (pixel, sub-pixel, domain).
+// ---------------------------------------------------------------------------
+template <int SHAPE, bool WIDE>
+__device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const float4* __restrict__ sch,
+                                                 double Sa, double Sb, double Sc) {
+    const float a_hi = __double2float_rn(Sa), b_hi = __double2float_rn(Sb), c_hi = __double2float_rn(Sc);
+    const float a_lo = __double2float_rn(Sa - (double)a_hi);
+    const float b_lo = __double2float_rn(Sb - (double)b_hi);
+    const float c_lo = __double2float_rn(Sc - (double)c_hi);
+    const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
+    const float* __restrict__ tab = static_cast<const float*>(P.table);
+    const float sHf = (float)P.sH, sKf = (float)P.sK;
+    double dacc = 0.0;
+    for (int w0 = 0; w0 < P.n_src; w0 += kChanChunk) {
+        const int we = min(P.n_src, w0 + kChanChunk);
+        float accf = 0.0f;
+#pragma unroll 2
+        for (int w = w0; w < we; ++w) {
+            const float4 c = sch[w];
+            const AxisF32 A = axis_f32(a_hi, a_lo, c.x, c.y, Na);
+            const AxisF32 B = axis_f32(b_hi, b_lo, c.x, c.y, Nb);
+            const AxisF32 C = axis_f32(c_hi, c_lo, c.x, c.y, Nc);
+            float L2;
+            if constexpr (SHAPE == 0) {
+                const float nn = (A.num * B.num) * C.num;
+                const float dd = (A.den * B.den) * C.den;
+                const float ratio = nn * rcp_approx_f32(dd);
+                L2 = ratio * ratio;
+            } else {
+                const float x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
+                L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn_f);
+            }
+            float F2;
+            if constexpr (!WIDE) {
+                // exact integer arithmetic in the FP32 significand; the biased
+                // float's bit pattern is the (offset) table index
+                const float fi = __fmaf_rn(A.n, sHf, __fmaf_rn(B.n, sKf, C.n + P.magic_cf));
+                F2 = __ldg(tab + __float_as_uint(fi));
+            } else {
+                const int idx = (__float2int_rn(A.n) - P.lo[0]) * P.sH +
+                                (__float2int_rn(B.n) - P.lo[1]) * P.sK + (__float2int_rn(C.n) - P.lo[2]);
+                F2 = __ldg(tab + idx);
+            }
+            accf = __fmaf_rn(F2 * c.z, L2, accf);
+        }
+        dacc += (double)accf;
+    }
+    return dacc;
+}
+
+template <int SHAPE, bool WIDE>
+__device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
+                                                 double Sa, double Sb, double Sc) {
+    const double Na = P.n_cells_d[0], Nb = P.n_cells_d[1], Nc = P.n_cells_d[2];
+    const double* __restrict__ tab = static_cast<const double*>(P.table);
+    const double sHd = (double)P.sH, sKd = (double)P.sK;
+    double acc = 0.0;
+#pragma unroll 2
+    for (int w = 0; w < P.n_src; ++w) {
+        const double2 c = sch[w];
+        const AxisF64 A = axis_f64(Sa, c.x, Na);
+        const AxisF64 B = axis_f64(Sb, c.x, Nb);
+        const AxisF64 C = axis_f64(Sc, c.x, Nc);
+        double L2;
+        if constexpr (SHAPE == 0) {
+            const double nn = (A.num * B.num) * C.num;
+            const double dd = (A.den * B.den) * C.den;
+            const double ratio = nn * rcp_f64(dd);
+            L2 = ratio * ratio;
+        } else {
+            const double x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
+            L2 = shape_latt2<SHAPE, double>(x * x + y * y + z * z, P.nnn_d);
+        }
+        double F2;
+        if constexpr (!WIDE) {
+            const double di = __fma_rn(A.n, sHd, __fma_rn(B.n, sKd, C.n + P.magic_cd));
+            F2 = __ldg(tab + __double2loint(di));
+        } else {
+            const int idx = (__double2int_rn(A.n) - P.lo[0]) * P.sH +
+                            (__double2int_rn(B.n) - P.lo[1]) * P.sK + (__double2int_rn(C.n) - P.lo[2]);
+            F2 = __ldg(tab + idx);
+        }
+        acc = __fma_rn(F2 * c.y, L2, acc);
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path.
+// ---------------------------------------------------------------------------
+template <int COMPUTE, int SHAPE, bool WIDE>
+__global__ void __launch_bounds__(kBlockX* kBlockY) spots_kernel(const SpotsParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.y * kBlockX + threadIdx.x;
+    if constexpr (COMPUTE == 1) {
+        float4* s = reinterpret_cast<float4*>(smem_raw);
+        const float4* g = static_cast<const float4*>(P.chan);
+        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
+    } else {
+        double2* s = reinterpret_cast<double2*>(smem_raw);
+        const double2* g = static_cast<const double2*>(P.chan);
+        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
+    }
+    __syncthreads();
+
+    const DevPanel& pan = P.panels[blockIdx.z];
+    const int f = blockIdx.x * kBlockX + threadIdx.x;
+    const int sl = blockIdx.y * kBlockY + threadIdx.y;
+    if (sl >= pan.slow || f >= pan.fast) return;
+
+    const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
+    const double ps = pan.pixel_size;
+    const int os = P.oversample;
+    const double dos = (double)os;
+    double acc = 0.0;
+
+    for (int i = 0; i < os; ++i) {
+        // kernels.py:169,177: s_coord = ((slow + (i + 0.5)/os) - bc_s) * ps
+        const double s_coord = (((double)sl + ((double)i + 0.5) / dos) - pan.bc_slow) * ps;
+        for (int j = 0; j < os; ++j) {
+            const double f_coord = (((double)f + ((double)j + 0.5) / dos) - pan.bc_fast) * ps;
+            // kernels.py:179-183: pos = d*beam + s*slow_axis + f*fast_axis
+            const double p0 = pan.distance * b0 + s_coord * pan.slow_axis[0] + f_coord * pan.fast_axis[0];
+            const double p1 = pan.distance * b1 + s_coord * pan.slow_axis[1] + f_coord * pan.fast_axis[1];
+            const double p2 = pan.distance * b2 + s_coord * pan.slow_axis[2] + f_coord * pan.fast_axis[2];
+            for (int th = 0; th < pan.thick_steps; ++th) {
+                const double depth = (double)th * pan.thick_step;  // X1 parallax layer
+                const double q0 = p0 + depth * pan.odet[0];
+                const double q1 = p1 + depth * pan.odet[1];
+                const double q2 = p2 + depth * pan.odet[2];
+                // kernels.py:185-191
+                const double r2 = q0 * q0 + q1 * q1 + q2 * q2;
+                const double r = sqrt(r2);
+                const double s0 = q0 / r, s1 = q1 / r, s2 = q2 / r;
+                const double cos_obl = fabs(s0 * pan.normal[0] + s1 * pan.normal[1] + s2 * pan.normal[2]);
+                double factor = (ps * ps / r2) * cos_obl;
+                if (P.pol_on) {  // kernels.py:197-201
+                    const double c2t = fmin(fmax(s0 * b0 + s1 * b1 + s2 * b2, -1.0), 1.0);
+                    factor *= 0.5 * (1.0 + c2t * c2t);
+                }
+                if (pan.thick_step > 0.0) {
+                    // absorbed fraction of layer th along the ray (nanoBragg capture fraction)
+                    const double par = fabs(s0 * pan.odet[0] + s1 * pan.odet[1] + s2 * pan.odet[2]);
+                    const double mu = pan.inv_atten / par;
+                    factor *= exp(-depth * mu) - exp(-(depth + pan.thick_step) * mu);
+                }
+                // kernels.py:234: rel = s_out - beam; h = rel . a / lambda
+                const double r0 = s0 - b0, r1 = s1 - b1, rr2 = s2 - b2;
+                double sub = 0.0;
+                for (int d = 0; d < P.n_dom; ++d) {
+                    const double* B = P.bases + 9 * d;
+                    const double Sa = r0 * __ldg(B + 0) + r1 * __ldg(B + 1) + rr2 * __ldg(B + 2);
+                    const double Sb = r0 * __ldg(B + 3) + r1 * __ldg(B + 4) + rr2 * __ldg(B + 5);
+                    const double Sc = r0 * __ldg(B + 6) + r1 * __ldg(B + 7) + rr2 * __ldg(B + 8);
+                    if constexpr (COMPUTE == 1) {
+                        sub += domain_sum_f32<SHAPE, WIDE>(P, reinterpret_cast<const float4*>(smem_raw), Sa, Sb, Sc);
+                    } else {
+                        sub += domain_sum_f64<SHAPE, WIDE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
+                    }
+                }
+                acc += sub * factor;
+            }
+        }
+    }
+
+    // Fused epilogue: scale, store in the requested form, flag non-finite
+    // values (kernels.py:271-273, _store_checked :211-216).
+    const int64_t p = pan.out_offset + (int64_t)sl * pan.fast + f;
+    bool bad = false;
+    switch (P.out_mode) {
+        case kOutF32: {
+            const float v = (float)(P.out_scale * acc);
+            static_cast<float*>(P.out)[p] = v;
+            bad = !isfinite(v);
+            break;
+        }
+        case kOutF64: {
+            const double v = P.out_scale * acc;
+            static_cast<double*>(P.out)[p] = v;
+            bad = !isfinite(v);
+            break;
+        }
+        case kOutAddF64: {
+            const float v = (float)(P.out_scale * acc);
+            static_cast<double*>(P.out)[p] += (double)v;
+            bad = !isfinite(v);
+            break;
+        }
+        default: {  // raw partial for channel shards
+            static_cast<double*>(P.out)[p] += acc;
+            break;
+        }
+    }
+    if (bad) atomicMin(P.fault, (unsigned long long)p);
+}
+
+// ---------------------------------------------------------------------------
+// Epilogue-only kernels.
+// ---------------------------------------------------------------------------
+__global__ void finalize_kernel(const double* __restrict__ raw, int64_t n, double scale, int mode, void* out,
+                                unsigned long long* fault) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const double acc = raw[p];
+        bool bad;
+        if (mode == kOutF32) {
+            const float v = (float)(scale * acc);
+            static_cast<float*>(out)[p] = v;
+            bad = !isfinite(v);
+        } else if (mode == kOutF64) {
+            const double v = scale * acc;
+            static_cast<double*>(out)[p] = v;
+            bad = !isfinite(v);
+        } else {
+            const float v = (float)(scale * acc);
+            static_cast<double*>(out)[p] += (double)v;
+            bad = !isfinite(v);
+        }
+        if (bad) atomicMin(fault, (unsigned long long)p);
+    }
+}
+
+__global__ void add_array_kernel(double* __restrict__ lhs, const float* __restrict__ rhs, int64_t n) {
+    // kernels.py:327-328: lhs += float64(rhs); the upcast is exact, the add FP64
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        lhs[i] += (double)rhs[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launchers (C++ linkage, used by nbx_runtime.cu).
+// ---------------------------------------------------------------------------
+template <int COMPUTE, int SHAPE, bool WIDE>
+static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) {
+    auto k = spots_kernel<COMPUTE, SHAPE, WIDE>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    dim3 block(kBlockX, kBlockY, 1);
+    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow + kBlockY - 1) / kBlockY, P.n_panels);
+    k<<<grid, block, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <int COMPUTE, bool WIDE>
+static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cudaStream_t st) {
+    switch (shape) {
+        case 0: return launch_t<COMPUTE, 0, WIDE>(P, smem, st);
+        case 1: return launch_t<COMPUTE, 1, WIDE>(P, smem, st);
+        case 2: return launch_t<COMPUTE, 2, WIDE>(P, smem, st);
+        default: return launch_t<COMPUTE, 3, WIDE>(P, smem, st);
+    }
+}
+
+cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st) {
+    const size_t smem = (size_t)P.n_src * 16;
+    if (compute == 1) {
+        return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);
+    }
+    return wide ? launch_shape<0, true>(P, shape, smem, st) : launch_shape<0, false>(P, shape, smem, st);
+}
+
+static int grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
+                            unsigned long long* fault, cudaStream_t st) {
+    finalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(raw, n, scale, mode, out, fault);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStream_t st) {
+    add_array_kernel<<<grid_for(n, 256), 256, 0, st>>>(lhs, rhs, n);
+    return cudaGetLastError();
+}
+
+__global__ void noise_kernel(const void* __restrict__ mean, void* __restrict__ out, int64_t n, int dtype,
+                             uint64_t seed, uint64_t image) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const double mu = dtype ? static_cast<const double*>(mean)[p] : (double)static_cast<const float*>(mean)[p];
+        const double k = poisson_draw(mu, seed, image, (uint64_t)p);
+        if (dtype)
+            static_cast<double*>(out)[p] = k;
+        else
+            static_cast<float*>(out)[p] = (float)k;
+    }
+}
+
+cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
+                         cudaStream_t st) {
+    noise_kernel<<<grid_for(n, 256), 256, 0, st>>>(mean, out, n, dtype, seed, image);
+    return cudaGetLastError();
+}
+
+}  // namespace nbx

@@ -1,0 +1,55 @@
+// nbx_kernels.cuh -- device-side parameter blocks shared by the kernels and
+// the host runtime (nbx_runtime.cu).  Plain PODs, passed by value.
+#pragma once
+
+#include <cstdint>
+
+namespace nbx {
+
+// One panel as the kernel sees it: the reference's DetectorPanel
+// (model.py:328-371) with the per-panel constants hoisted.
+struct DevPanel {
+    int32_t slow, fast;            // pixels
+    int32_t thick_steps;           // >= 1
+    int32_t pad0;
+    int64_t out_offset;            // first output element of this panel
+    double pixel_size;
+    double distance;
+    double bc_slow, bc_fast;       // beam_center (slow, fast)
+    double fast_axis[3];
+    double slow_axis[3];
+    double normal[3];              // fast x slow (model.py:370-371): used for Omega
+    double odet[3];                // unit normal pointing away from the sample (thickness layers)
+    double thick_step;             // thickness / thick_steps (0: thin sensor)
+    double inv_atten;              // 1 / attenuation_length (0 when thin)
+};
+
+// Everything the spot kernel reads.  All pointers are device pointers.
+struct SpotsParams {
+    const DevPanel* panels;
+    int32_t n_panels;
+    int32_t oversample;
+    const double* bases;           // n_dom x 9, rows a, b, c
+    int32_t n_dom;
+    int32_t n_src;                 // channels in this launch (already sharded)
+    const void* chan;              // FP64: double2 {1/lambda, w}; FP32: float4 {iv_hi, iv_lo, w, 0}
+    const void* table;             // dense F^2 grid (FP32: scaled by sigma), biased base (see runtime)
+    double beam[3];
+    int32_t pol_on;
+    int32_t out_mode;              // NBX_OUT_*
+    double n_cells_d[3];
+    float n_cells_f[3];
+    float nnn_f;                   // Na*Nb*Nc
+    double nnn_d;
+    // dense-grid index: idx = (n_h - lo_h) * sH + (n_k - lo_k) * sK + (n_l - lo_l)
+    int32_t lo[3];
+    int32_t sH, sK;
+    float magic_cf;                // FP32 magic-index constant (see runtime)
+    double magic_cd;               // FP64 magic-index constant
+    double out_scale;              // r_e^2 fluence / norm (/ sigma on the FP32 path)
+    void* out;
+    unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none
+    int32_t max_slow, max_fast;
+};
+
+}  // namespace nbx

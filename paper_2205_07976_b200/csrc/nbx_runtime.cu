@@ -1,0 +1,730 @@
+// nbx_runtime.cu -- host runtime behind the C ABI in include/nbx.h.
+//
+// Owns: per-device contexts (streams, events, scratch), plan construction
+// (validation with the reference's error contract, the dense Fhkl grid sized
+// to the reachable Miller box, FP32 range scaling, channel/domain packing,
+// HBM upload) and the launches.  Nothing here throws across the ABI: every
+// entry point catches and converts to an NBX_* status + last-error string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/nbx.h"
+#include "nbx_kernels.cuh"
+#include "nbx_poisson.h"
+
+namespace nbx {
+cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st);
+cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
+                            unsigned long long* fault, cudaStream_t st);
+cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStream_t st);
+cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
+                         cudaStream_t st);
+}  // namespace nbx
+
+namespace {
+
+struct ArgError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define NBX_CUDA(call)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));               \
+    } while (0)
+
+// Device buffer that frees itself.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        release();
+        NBX_CUDA(cudaMalloc(&p, n));
+        bytes = n;
+    }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    DevBuf out_scratch;     // device image when the caller passes host memory
+    DevBuf fault;           // one u64
+    std::string err;
+};
+
+struct Plan {
+    Ctx* ctx = nullptr;
+    int compute = 0;
+    int shape = 0;
+    bool wide = false;
+    nbx::SpotsParams P{};
+    DevBuf panels, bases, chan, table;
+    int64_t n_pixels = 0;
+    int64_t steps = 0;
+    nbx_plan_info_t info{};
+    double scale = 0.0;      // r_e^2 fluence / norm
+    double out_scale = 0.0;  // scale / sigma
+    float last_ms = -1.f;
+    bool timed = false;
+};
+
+// --------------------------------------------------------------------------
+// Validation: mirrors the reference's constructors and kernel checks
+// (model.py:328-406, kernels.py:204-208) so the same bad inputs fail.
+// --------------------------------------------------------------------------
+bool finite(double x) { return std::isfinite(x); }
+
+double norm3(const double* v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
+
+void check_unit(const double* v, const char* what) {
+    for (int i = 0; i < 3; ++i)
+        if (!finite(v[i])) throw ArgError(std::string(what) + " must be finite");
+    if (std::fabs(norm3(v) - 1.0) > 1e-12) throw ArgError(std::string(what) + " must be a unit vector");
+}
+
+int64_t count_pixels(const nbx_spots_desc* d) {
+    if (!d || d->n_panels < 1 || !d->panels) throw ArgError("descriptor needs at least one panel");
+    int64_t n = 0;
+    for (int i = 0; i < d->n_panels; ++i) {
+        const nbx_panel& p = d->panels[i];
+        if (p.slow_pixels < 1 || p.fast_pixels < 1) throw ArgError("panel must have at least one pixel per axis");
+        n += (int64_t)p.slow_pixels * p.fast_pixels;
+    }
+    return n;
+}
+
+void validate(const nbx_spots_desc* d) {
+    count_pixels(d);
+    if (d->oversample < 1) throw ArgError("oversample must be >= 1");
+    for (int i = 0; i < d->n_panels; ++i) {
+        const nbx_panel& p = d->panels[i];
+        if (!(p.pixel_size > 0) || !finite(p.pixel_size)) throw ArgError("pixel_size must be > 0");
+        if (!(p.distance > 0) || !finite(p.distance)) throw ArgError("distance must be > 0");
+        if (!finite(p.beam_center[0]) || !finite(p.beam_center[1])) throw ArgError("beam_center must be finite");
+        check_unit(p.fast_axis, "fast_axis");
+        check_unit(p.slow_axis, "slow_axis");
+        const double dot = p.fast_axis[0] * p.slow_axis[0] + p.fast_axis[1] * p.slow_axis[1] +
+                           p.fast_axis[2] * p.slow_axis[2];
+        if (std::fabs(dot) > 1e-12) throw ArgError("fast_axis and slow_axis must be orthogonal");
+        if (p.thick_steps < 1) throw ArgError("thick_steps must be >= 1");
+        if (!(p.thickness >= 0) || !finite(p.thickness)) throw ArgError("thickness must be finite and >= 0");
+        if (p.thickness > 0 && !(p.attenuation_length > 0 && finite(p.attenuation_length)))
+            throw ArgError("attenuation_length must be > 0 when thickness > 0");
+    }
+    check_unit(d->beam_direction, "beam_direction");
+    if (d->n_sources < 1 || !d->wavelengths || !d->weights)
+        throw ArgError("spectrum needs at least one wavelength sample");
+    bool any_pos = false;
+    for (int i = 0; i < d->n_sources; ++i) {
+        if (!(d->wavelengths[i] > 0) || !finite(d->wavelengths[i])) throw ArgError("wavelengths must be > 0");
+        if (!finite(d->weights[i]) || d->weights[i] < 0) throw ArgError("weights must be finite and >= 0");
+        any_pos |= d->weights[i] > 0;
+    }
+    if (!any_pos && !(d->norm > 0)) throw ArgError("at least one sample must have weight > 0");
+    if (!finite(d->fluence) || d->fluence < 0) throw ArgError("fluence must be finite and >= 0");
+    if (!finite(d->r_e_sqr)) throw ArgError("r_e_sqr must be finite");
+    if (d->n_domains < 1 || !d->bases) throw ArgError("mosaic rotations must be a non-empty (n, 3, 3) array");
+    for (int i = 0; i < 9 * d->n_domains; ++i)
+        if (!finite(d->bases[i])) throw ArgError("rotated bases must be finite");
+    for (int a = 0; a < 3; ++a)
+        if (d->n_cells[a] < 1) throw ArgError("n_cells must all be >= 1");
+    if (d->shape < 0 || d->shape > 3) throw ArgError("unknown shape transform");
+    if (d->n_entries < 0 || (d->n_entries > 0 && (!d->hkl || !d->amplitudes)))
+        throw ArgError("structure-factor table arrays missing");
+    for (int i = 0; i < d->n_entries; ++i) {
+        const double f = d->amplitudes[i];
+        if (!finite(f) || f < 0) throw ArgError("amplitudes must be finite and >= 0");
+        for (int a = 0; a < 3; ++a)
+            if (std::abs((int64_t)d->hkl[3 * i + a]) >= (1 << 20)) throw ArgError("Miller index out of supported range");
+    }
+    if (!finite(d->default_f) || d->default_f < 0) throw ArgError("default_f must be finite and non-negative");
+    const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
+    if (sb < 0 || se > d->n_sources || sb >= se) throw ArgError("invalid source shard range");
+}
+
+// Largest |s_out - beam| over every sub-pixel / layer position of every panel.
+// The set {x : angle(x, beam) <= alpha} is a convex cone for alpha < 90 deg, so
+// the maximum over a (slab of a) rectangle is attained at one of its corners.
+double max_rel(const nbx_spots_desc* d) {
+    const double* b = d->beam_direction;
+    double min_cos = 1.0;
+    for (int i = 0; i < d->n_panels; ++i) {
+        const nbx_panel& p = d->panels[i];
+        double nrm[3] = {p.fast_axis[1] * p.slow_axis[2] - p.fast_axis[2] * p.slow_axis[1],
+                         p.fast_axis[2] * p.slow_axis[0] - p.fast_axis[0] * p.slow_axis[2],
+                         p.fast_axis[0] * p.slow_axis[1] - p.fast_axis[1] * p.slow_axis[0]};
+        const double sgn = (nrm[0] * b[0] + nrm[1] * b[1] + nrm[2] * b[2]) < 0 ? -1.0 : 1.0;
+        const double depth_max = p.thickness > 0 ? p.thickness : 0.0;
+        for (int c = 0; c < 8; ++c) {
+            const double s = ((c & 1) ? (double)p.slow_pixels : 0.0) - p.beam_center[0];
+            const double f = ((c & 2) ? (double)p.fast_pixels : 0.0) - p.beam_center[1];
+            const double dep = (c & 4) ? depth_max : 0.0;
+            double q[3];
+            for (int a = 0; a < 3; ++a)
+                q[a] = p.distance * b[a] + s * p.pixel_size * p.slow_axis[a] + f * p.pixel_size * p.fast_axis[a] +
+                       dep * sgn * nrm[a];
+            const double cs = (q[0] * b[0] + q[1] * b[1] + q[2] * b[2]) / norm3(q);
+            min_cos = std::min(min_cos, cs);
+        }
+    }
+    if (min_cos <= 0.02) return 2.0;
+    return std::sqrt(std::max(0.0, 2.0 - 2.0 * min_cos)) * (1.0 + 1e-9) + 1e-12;
+}
+
+Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
+    validate(d);
+    if (compute != NBX_COMPUTE_FP64 && compute != NBX_COMPUTE_FP32) throw ArgError("unknown compute path");
+    auto plan = new Plan();
+    try {
+        plan->ctx = ctx;
+        plan->compute = compute;
+        plan->shape = d->shape;
+        nbx::SpotsParams& P = plan->P;
+        const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
+        const int n_src = se - sb;
+        const int os = d->oversample;
+
+        // normalisation and scale (kernels.py:242-245)
+        double norm = d->norm;
+        if (!(norm > 0)) {
+            double wsum = 0.0;
+            for (int i = 0; i < d->n_sources; ++i) wsum += d->weights[i];
+            norm = wsum * (double)d->n_domains * (double)(os * os);
+        }
+        plan->scale = d->r_e_sqr * d->fluence / norm;
+
+        // panels
+        std::vector<nbx::DevPanel> hp(d->n_panels);
+        int64_t off = 0;
+        int max_slow = 0, max_fast = 0;
+        int64_t sub_steps = 0;
+        for (int i = 0; i < d->n_panels; ++i) {
+            const nbx_panel& s = d->panels[i];
+            nbx::DevPanel& t = hp[i];
+            std::memset(&t, 0, sizeof(t));
+            t.slow = s.slow_pixels;
+            t.fast = s.fast_pixels;
+            t.out_offset = off;
+            t.pixel_size = s.pixel_size;
+            t.distance = s.distance;
+            t.bc_slow = s.beam_center[0];
+            t.bc_fast = s.beam_center[1];
+            for (int a = 0; a < 3; ++a) {
+                t.fast_axis[a] = s.fast_axis[a];
+                t.slow_axis[a] = s.slow_axis[a];
+            }
+            t.normal[0] = s.fast_axis[1] * s.slow_axis[2] - s.fast_axis[2] * s.slow_axis[1];
+            t.normal[1] = s.fast_axis[2] * s.slow_axis[0] - s.fast_axis[0] * s.slow_axis[2];
+            t.normal[2] = s.fast_axis[0] * s.slow_axis[1] - s.fast_axis[1] * s.slow_axis[0];
+            const double* b = d->beam_direction;
+            const double sgn = (t.normal[0] * b[0] + t.normal[1] * b[1] + t.normal[2] * b[2]) < 0 ? -1.0 : 1.0;
+            for (int a = 0; a < 3; ++a) t.odet[a] = sgn * t.normal[a];
+            if (s.thickness > 0) {
+                t.thick_steps = s.thick_steps;
+                t.thick_step = s.thickness / (double)s.thick_steps;
+                t.inv_atten = 1.0 / s.attenuation_length;
+            } else {
+                t.thick_steps = 1;  // a thin sensor has exactly one layer (reference)
+                t.thick_step = 0.0;
+                t.inv_atten = 0.0;
+            }
+            const int64_t npx = (int64_t)s.slow_pixels * s.fast_pixels;
+            off += npx;
+            sub_steps += npx * (int64_t)(os * os) * t.thick_steps;
+            max_slow = std::max(max_slow, s.slow_pixels);
+            max_fast = std::max(max_fast, s.fast_pixels);
+        }
+        plan->n_pixels = off;
+        plan->steps = sub_steps * (int64_t)n_src * d->n_domains;
+
+        // reachable Miller box (+1 margin for rounding) -> dense grid
+        const double relmax = max_rel(d);
+        double ivmax = 0.0;
+        for (int i = sb; i < se; ++i) ivmax = std::max(ivmax, 1.0 / d->wavelengths[i]);
+        int hmax[3];
+        for (int a = 0; a < 3; ++a) {
+            double m = 0.0;
+            for (int dd = 0; dd < d->n_domains; ++dd) m = std::max(m, norm3(d->bases + 9 * dd + 3 * a));
+            const double hb = std::ceil(m * relmax * ivmax) + 1.0;
+            if (hb > (double)(1 << 20)) throw ArgError("reachable Miller range exceeds the supported |index| < 2^20");
+            hmax[a] = (int)hb;
+        }
+        const int64_t dims[3] = {2 * (int64_t)hmax[0] + 1, 2 * (int64_t)hmax[1] + 1, 2 * (int64_t)hmax[2] + 1};
+        const int64_t cells = dims[0] * dims[1] * dims[2];
+        if (cells > (int64_t(1) << 30))
+            throw ArgError("reachable Miller box too large for the dense Fhkl grid (" + std::to_string(cells) +
+                           " cells)");
+        for (int a = 0; a < 3; ++a) P.lo[a] = -hmax[a];
+        P.sK = (int32_t)dims[2];
+        P.sH = (int32_t)(dims[1] * dims[2]);
+        const bool wide32 = cells > (int64_t(1) << 22);
+        plan->wide = (compute == NBX_COMPUTE_FP32) ? wide32 : false;
+
+        // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma)
+        const double def2 = d->default_f * d->default_f;
+        std::vector<double> f2(cells, def2);
+        double maxf2 = def2;
+        for (int i = 0; i < d->n_entries; ++i) {
+            const int h = d->hkl[3 * i], k = d->hkl[3 * i + 1], l = d->hkl[3 * i + 2];
+            if (std::abs(h) > hmax[0] || std::abs(k) > hmax[1] || std::abs(l) > hmax[2]) continue;  // unreachable
+            const double F = d->amplitudes[i];
+            const int64_t idx = (int64_t)(h + hmax[0]) * P.sH + (int64_t)(k + hmax[1]) * P.sK + (l + hmax[2]);
+            f2[idx] = F * F;
+            maxf2 = std::max(maxf2, F * F);
+        }
+        double sigma = 1.0;
+        if (compute == NBX_COMPUTE_FP32) {
+            double maxw = 0.0;
+            for (int i = sb; i < se; ++i) maxw = std::max(maxw, d->weights[i]);
+            const double nnn = (double)d->n_cells[0] * d->n_cells[1] * d->n_cells[2];
+            const double peak = maxf2 * maxw * nnn * nnn;
+            if (peak > 0 && finite(peak)) {
+                int e = (int)std::floor(100.0 - std::log2(peak));
+                e = std::max(-1000, std::min(e, 100));
+                sigma = std::ldexp(1.0, e);
+            }
+        }
+        plan->out_scale = plan->scale / sigma;
+
+        // channels
+        if (compute == NBX_COMPUTE_FP32) {
+            std::vector<float> ch(4 * (size_t)n_src);
+            for (int i = 0; i < n_src; ++i) {
+                const double iv = 1.0 / d->wavelengths[sb + i];  // kernels.py:257
+                const float hi = (float)iv;
+                ch[4 * i + 0] = hi;
+                ch[4 * i + 1] = (float)(iv - (double)hi);
+                ch[4 * i + 2] = (float)d->weights[sb + i];
+                ch[4 * i + 3] = 0.f;
+            }
+            plan->chan.ensure(ch.size() * sizeof(float));
+            NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(float), cudaMemcpyHostToDevice));
+            std::vector<float> tf(cells);
+            for (int64_t i = 0; i < cells; ++i) tf[i] = (float)(f2[i] * sigma);
+            plan->table.ensure(cells * sizeof(float));
+            NBX_CUDA(cudaMemcpy(plan->table.p, tf.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
+        } else {
+            std::vector<double> ch(2 * (size_t)n_src);
+            for (int i = 0; i < n_src; ++i) {
+                ch[2 * i + 0] = 1.0 / d->wavelengths[sb + i];
+                ch[2 * i + 1] = d->weights[sb + i];
+            }
+            plan->chan.ensure(ch.size() * sizeof(double));
+            NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice));
+            plan->table.ensure(cells * sizeof(double));
+            NBX_CUDA(cudaMemcpy(plan->table.p, f2.data(), cells * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        if ((size_t)n_src * 16 > 200 * 1024) throw ArgError("too many sources in one shard (max 12800)");
+
+        plan->bases.ensure(sizeof(double) * 9 * d->n_domains);
+        NBX_CUDA(cudaMemcpy(plan->bases.p, d->bases, sizeof(double) * 9 * d->n_domains, cudaMemcpyHostToDevice));
+        plan->panels.ensure(sizeof(nbx::DevPanel) * hp.size());
+        NBX_CUDA(cudaMemcpy(plan->panels.p, hp.data(), sizeof(nbx::DevPanel) * hp.size(), cudaMemcpyHostToDevice));
+
+        // kernel parameter block
+        P.panels = static_cast<const nbx::DevPanel*>(plan->panels.p);
+        P.n_panels = d->n_panels;
+        P.oversample = os;
+        P.bases = static_cast<const double*>(plan->bases.p);
+        P.n_dom = d->n_domains;
+        P.n_src = n_src;
+        P.chan = plan->chan.p;
+        for (int a = 0; a < 3; ++a) {
+            P.beam[a] = d->beam_direction[a];
+            P.n_cells_d[a] = (double)d->n_cells[a];
+            P.n_cells_f[a] = (float)d->n_cells[a];
+        }
+        P.nnn_d = (double)d->n_cells[0] * d->n_cells[1] * d->n_cells[2];
+        P.nnn_f = (float)P.nnn_d;
+        P.pol_on = d->polarization_on ? 1 : 0;
+        // magic-index constants: all partial sums stay in [M, M + cells)
+        const double part = -(double)P.lo[0] * P.sH - (double)P.lo[1] * P.sK - (double)P.lo[2];
+        P.magic_cf = (float)(12582912.0 + part);          // 1.5 * 2^23
+        P.magic_cd = 6755399441055744.0 + part;           // 1.5 * 2^52
+        if (compute == NBX_COMPUTE_FP32 && !plan->wide) {
+            // index = float bits - 0x4B400000: bias the base pointer instead
+            P.table = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(plan->table.p) -
+                                                    (uintptr_t)0x4B400000u * sizeof(float));
+        } else {
+            P.table = plan->table.p;
+        }
+        P.max_slow = max_slow;
+        P.max_fast = max_fast;
+        P.out_scale = plan->out_scale;
+
+        nbx_plan_info_t& I = plan->info;
+        I.n_pixels = plan->n_pixels;
+        I.steps = plan->steps;
+        I.table_cells = cells;
+        for (int a = 0; a < 3; ++a) {
+            I.table_lo[a] = P.lo[a];
+            I.table_dim[a] = (int32_t)dims[a];
+        }
+        I.compute = compute;
+        I.table_kind = plan->wide ? 1 : 0;
+        I.scale = plan->scale;
+        return plan;
+    } catch (...) {
+        delete plan;
+        throw;
+    }
+}
+
+size_t out_elem_bytes(int mode) { return mode == NBX_OUT_F32 ? 4 : 8; }
+
+void check_mode(int mode) {
+    if (mode < NBX_OUT_F32 || mode > NBX_OUT_RAW_F64) throw ArgError("unknown output mode");
+}
+
+// Run a plan into `out`; returns the lowest non-finite pixel or -1.
+int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
+    check_mode(mode);
+    if (!out) throw ArgError("output buffer is NULL");
+    Ctx* ctx = plan->ctx;
+    NBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const size_t bytes = (size_t)plan->n_pixels * out_elem_bytes(mode);
+    void* dout = out;
+    if (!on_device) {
+        ctx->out_scratch.ensure(bytes);
+        dout = ctx->out_scratch.p;
+        if (mode == NBX_OUT_ADD_F64 || mode == NBX_OUT_RAW_F64)
+            NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, st));
+    }
+    ctx->fault.ensure(sizeof(unsigned long long));
+    NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, sizeof(unsigned long long), st));
+    nbx::SpotsParams P = plan->P;
+    P.out_mode = mode;
+    P.out = dout;
+    P.fault = static_cast<unsigned long long*>(ctx->fault.p);
+    NBX_CUDA(cudaEventRecord(ctx->ev0, st));
+    NBX_CUDA(nbx::launch_spots(P, plan->compute, plan->shape, plan->wide, st));
+    NBX_CUDA(cudaEventRecord(ctx->ev1, st));
+    plan->timed = true;
+    unsigned long long fault = ~0ull;
+    NBX_CUDA(cudaMemcpyAsync(&fault, ctx->fault.p, sizeof(fault), cudaMemcpyDeviceToHost, st));
+    if (!on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
+    NBX_CUDA(cudaStreamSynchronize(st));
+    NBX_CUDA(cudaEventElapsedTime(&plan->last_ms, ctx->ev0, ctx->ev1));
+    return fault == ~0ull ? -1 : (int64_t)fault;
+}
+
+thread_local std::string g_noctx_err;
+
+void set_err(void* ctxp, const std::string& msg) {
+    if (ctxp)
+        static_cast<Ctx*>(ctxp)->err = msg;
+    else
+        g_noctx_err = msg;
+}
+
+template <typename F>
+int guarded(void* ctxp, F&& f) {
+    try {
+        return f();
+    } catch (const ArgError& e) {
+        set_err(ctxp, e.what());
+        return NBX_ERR_ARG;
+    } catch (const CudaError& e) {
+        set_err(ctxp, e.what());
+        return NBX_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        set_err(ctxp, "host allocation failed");
+        return NBX_ERR_ARG;
+    } catch (const std::exception& e) {
+        set_err(ctxp, e.what());
+        return NBX_ERR_CUDA;
+    }
+}
+
+int fault_status(void* ctxp, int64_t bad, int64_t* first_bad) {
+    if (first_bad) *first_bad = bad;
+    if (bad >= 0) {
+        set_err(ctxp, "non-finite value at pixel " + std::to_string(bad));
+        return NBX_ERR_NUMERICAL;
+    }
+    return NBX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nbx_version(void) { return NBX_VERSION; }
+
+void* nbx_ctx_create(int device) {
+    try {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            g_noctx_err = "no CUDA device available";
+            return nullptr;
+        }
+        if (device < 0 || device >= n) {
+            g_noctx_err = "device index out of range";
+            return nullptr;
+        }
+        auto ctx = new Ctx();
+        ctx->device = device;
+        if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+            g_noctx_err = std::string("CUDA init failed: ") + cudaGetErrorString(cudaGetLastError());
+            delete ctx;
+            return nullptr;
+        }
+        ctx->stream = ctx->own;
+        return ctx;
+    } catch (...) {
+        g_noctx_err = "context allocation failed";
+        return nullptr;
+    }
+}
+
+void nbx_ctx_destroy(void* ctxp) {
+    if (!ctxp) return;
+    Ctx* ctx = static_cast<Ctx*>(ctxp);
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->out_scratch.release();
+    ctx->fault.release();
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+const char* nbx_last_error(void* ctxp) {
+    if (!ctxp) return g_noctx_err.c_str();
+    return static_cast<Ctx*>(ctxp)->err.c_str();
+}
+
+int nbx_ctx_set_stream(void* ctxp, void* stream) {
+    if (!ctxp) return NBX_ERR_ARG;
+    Ctx* ctx = static_cast<Ctx*>(ctxp);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return NBX_OK;
+}
+
+int nbx_ctx_synchronize(void* ctxp) {
+    return guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        NBX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return NBX_OK;
+    });
+}
+
+int64_t nbx_output_pixels(const nbx_spots_desc* d) {
+    try {
+        return count_pixels(d);
+    } catch (...) {
+        return -1;
+    }
+}
+
+void* nbx_plan_create(void* ctxp, const nbx_spots_desc* d, int compute) {
+    Plan* plan = nullptr;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        plan = build_plan(static_cast<Ctx*>(ctxp), d, compute);
+        return NBX_OK;
+    });
+    return st == NBX_OK ? plan : nullptr;
+}
+
+int nbx_plan_run(void* planp, int out_mode, void* out, int out_on_device, int64_t* first_bad) {
+    if (!planp) return NBX_ERR_ARG;
+    Plan* plan = static_cast<Plan*>(planp);
+    int64_t bad = -1;
+    int st = guarded(plan->ctx, [&] {
+        bad = run_plan(plan, out_mode, out, out_on_device);
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    return fault_status(plan->ctx, bad, first_bad);
+}
+
+int nbx_plan_info(void* planp, nbx_plan_info_t* info) {
+    if (!planp || !info) return NBX_ERR_ARG;
+    *info = static_cast<Plan*>(planp)->info;
+    return NBX_OK;
+}
+
+double nbx_plan_last_kernel_ms(void* planp) {
+    if (!planp) return -1.0;
+    return static_cast<Plan*>(planp)->last_ms;
+}
+
+void nbx_plan_destroy(void* planp) {
+    if (!planp) return;
+    Plan* plan = static_cast<Plan*>(planp);
+    cudaSetDevice(plan->ctx->device);
+    cudaStreamSynchronize(plan->ctx->stream);
+    delete plan;
+}
+
+int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, void* out, int out_on_device,
+              int64_t* first_bad) {
+    int64_t bad = -1;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        check_mode(out_mode);
+        Plan* plan = build_plan(static_cast<Ctx*>(ctxp), d, compute);
+        try {
+            bad = run_plan(plan, out_mode, out, out_on_device);
+        } catch (...) {
+            delete plan;
+            throw;
+        }
+        delete plan;
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    return fault_status(ctxp, bad, first_bad);
+}
+
+int nbx_spots_batch(void* ctxp, const nbx_spots_desc* descs, int n_images, int compute, int out_mode,
+                    void* const* outs, int out_on_device, int64_t* first_bad) {
+    if (first_bad) *first_bad = -1;
+    if (n_images < 0 || (n_images > 0 && (!descs || !outs))) {
+        set_err(ctxp, "invalid batch arguments");
+        return NBX_ERR_ARG;
+    }
+    for (int i = 0; i < n_images; ++i) {
+        int64_t bad = -1;
+        const int st = nbx_spots(ctxp, descs + i, compute, out_mode, outs[i], out_on_device, &bad);
+        if (st != NBX_OK) {
+            // report (image, pixel) as image * 2^40 + pixel so callers can locate it
+            if (first_bad && bad >= 0) *first_bad = ((int64_t)i << 40) | bad;
+            return st;
+        }
+    }
+    return NBX_OK;
+}
+
+int nbx_finalize(void* ctxp, const double* raw, int64_t n, double scale, int out_mode, void* out, int out_on_device,
+                 int64_t* first_bad) {
+    int64_t bad = -1;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        if (!raw || !out || n < 0) throw ArgError("invalid finalize arguments");
+        if (out_mode == NBX_OUT_RAW_F64) throw ArgError("finalize cannot write a raw image");
+        check_mode(out_mode);
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const size_t bytes = (size_t)n * out_elem_bytes(out_mode);
+        void* dout = out;
+        if (!out_on_device) {
+            ctx->out_scratch.ensure(bytes);
+            dout = ctx->out_scratch.p;
+            if (out_mode == NBX_OUT_ADD_F64) NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, s));
+        }
+        ctx->fault.ensure(8);
+        NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 8, s));
+        NBX_CUDA(nbx::launch_finalize(raw, n, scale, out_mode, dout, static_cast<unsigned long long*>(ctx->fault.p), s));
+        unsigned long long f = ~0ull;
+        NBX_CUDA(cudaMemcpyAsync(&f, ctx->fault.p, 8, cudaMemcpyDeviceToHost, s));
+        if (!out_on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        bad = f == ~0ull ? -1 : (int64_t)f;
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    return fault_status(ctxp, bad, first_bad);
+}
+
+int nbx_add_array(void* ctxp, double* lhs, const float* rhs, int64_t n, int on_device) {
+    return guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        if (n < 0 || (n > 0 && (!lhs || !rhs))) throw ArgError("invalid add_array arguments");
+        if (n == 0) return NBX_OK;
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        if (on_device) {
+            NBX_CUDA(nbx::launch_add_array(lhs, rhs, n, s));
+            NBX_CUDA(cudaStreamSynchronize(s));
+            return NBX_OK;
+        }
+        DevBuf dl, dr;
+        dl.ensure((size_t)n * 8);
+        dr.ensure((size_t)n * 4);
+        NBX_CUDA(cudaMemcpyAsync(dl.p, lhs, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        NBX_CUDA(cudaMemcpyAsync(dr.p, rhs, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+        NBX_CUDA(nbx::launch_add_array(static_cast<double*>(dl.p), static_cast<const float*>(dr.p), n, s));
+        NBX_CUDA(cudaMemcpyAsync(lhs, dl.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        return NBX_OK;
+    });
+}
+
+int nbx_add_noise(void* ctxp, const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
+                  int on_device) {
+    return guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        if (dtype != 0 && dtype != 1) throw ArgError("dtype must be 0 (f32) or 1 (f64)");
+        if (n < 0 || (n > 0 && (!mean || !out))) throw ArgError("invalid noise arguments");
+        if (n == 0) return NBX_OK;
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const size_t bytes = (size_t)n * (dtype ? 8 : 4);
+        if (on_device) {
+            NBX_CUDA(nbx::launch_noise(mean, out, n, dtype, seed, image, s));
+            NBX_CUDA(cudaStreamSynchronize(s));
+            return NBX_OK;
+        }
+        DevBuf dm, dout;
+        dm.ensure(bytes);
+        dout.ensure(bytes);
+        NBX_CUDA(cudaMemcpyAsync(dm.p, mean, bytes, cudaMemcpyHostToDevice, s));
+        NBX_CUDA(nbx::launch_noise(dm.p, dout.p, n, dtype, seed, image, s));
+        NBX_CUDA(cudaMemcpyAsync(out, dout.p, bytes, cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        return NBX_OK;
+    });
+}
+
+int nbx_poisson_host(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image) {
+    if (dtype != 0 && dtype != 1) return NBX_ERR_ARG;
+    if (n < 0 || (n > 0 && (!mean || !out))) return NBX_ERR_ARG;
+    for (int64_t p = 0; p < n; ++p) {
+        const double mu = dtype ? static_cast<const double*>(mean)[p] : (double)static_cast<const float*>(mean)[p];
+        const double k = nbx::poisson_draw(mu, seed, image, (uint64_t)p);
+        if (dtype)
+            static_cast<double*>(out)[p] = k;
+        else
+            static_cast<float*>(out)[p] = (float)k;
+    }
+    return NBX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+"""The C-ABI library builds, loads and exports exactly what include/nbx.h declares (CPU-only)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2205_07976_b200 import _native, build
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _native.load()
+
+
+def header_functions():
+    text = (ROOT / "include" / "nbx.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(nbx_\w+)\s*\(", text))
+
+
+def test_header_matches_binding_table():
+    assert header_functions() == set(_native.EXPORTS)
+
+
+def test_every_symbol_exported(lib):
+    for name in _native.EXPORTS:
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a_only():
+    out = __import__("subprocess").run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)],
+                                       capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_version(lib):
+    assert lib.nbx_version() == 10000
+
+
+def test_no_gpu_fails_loudly_here(lib):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    assert not lib.nbx_ctx_create(0)
+    assert b"device" in lib.nbx_last_error(None)
+    with pytest.raises(_native.NativeError):
+        _native.Context(0)
+    _native._lib = None  # first use through context() must not deadlock on the loader lock
+    with pytest.raises(_native.NativeError):
+        _native.context(0)
+
+
+def test_output_pixels_is_host_only(lib):
+    from paper_2205_07976_b200 import synthetic
+
+    desc = __import__("paper_2205_07976_b200").describe(synthetic.c1_context())
+    assert lib.nbx_output_pixels(C.byref(desc.c)) == 256 * 256
+
+
+def test_struct_layout_matches_header():
+    # offsets the C compiler gives nbx_spots_desc, checked via a tiny C probe
+    import subprocess
+    import tempfile
+
+    probe = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "nbx.h"
+int main(){printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(nbx_panel), sizeof(nbx_spots_desc),
+ offsetof(nbx_spots_desc, bases), offsetof(nbx_spots_desc, default_f), offsetof(nbx_spots_desc, src_end),
+ sizeof(nbx_plan_info_t), offsetof(nbx_panel, attenuation_length));return 0;}
+'''
+    with tempfile.TemporaryDirectory() as d:
+        src = Path(d) / "p.c"
+        src.write_text(probe)
+        exe = Path(d) / "p"
+        subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+        got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [C.sizeof(_native.Panel), C.sizeof(_native.SpotsDesc), _native.SpotsDesc.bases.offset,
+            _native.SpotsDesc.default_f.offset, _native.SpotsDesc.src_end.offset, C.sizeof(_native.PlanInfo),
+            _native.Panel.attenuation_length.offset]
+    assert got == want
+
+
+def test_host_poisson_twin_matches_oracle_build(lib):
+    """nbx_poisson_host (product .so, nvcc host build) == oracle build (g++): same header, same bits."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(5)
+    mean = np.concatenate([rng.uniform(0, 15, 4000), rng.uniform(15, 1e5, 4000), [0.0, -1.0, 1e9]])
+    out = np.empty_like(mean)
+    assert lib.nbx_poisson_host(mean.ctypes.data, out.ctypes.data, mean.size, 1, 77, 3) == 0
+    assert np.array_equal(out, oracle.poisson(mean, 77, 3))

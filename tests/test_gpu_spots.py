@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a spot kernel through the C ABI vs the reference's outputs and the oracle.
+
+Tolerances (BASELINE.json north_star): FP64 path 1e-9 relative
+on total and per-spot intensity; FP32 path 1e-4.  Extensions without a
+reference (thickness, shapes, phi, multi-panel, channel shards) are checked
+against the CPU oracle (oracle/) at the FP64 tolerance.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import parity
+from oracle import oracle
+from paper_2205_07976_b200 import (
+    R_E_SQR,
+    BeamSpectrum,
+    Detector,
+    DetectorPanel,
+    Executor,
+    NumericalFault,
+    PatternFault,
+    PhiScan,
+    PixelBuffer,
+    ShapeMismatchError,
+    SpotsContext,
+    SpotsPlan,
+    add_array,
+    add_noise,
+    describe,
+    nanobragg_spots,
+    pixel_lab_position,
+    solid_angle,
+    synthetic,
+)
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["thomson", "scalar_match", "triclinic_pol_2wl", "pipeline_spots", "c1_toy", "tilted", "ls49_centre",
+         "ls49_edge"]
+FP64_TOL = 1e-9
+FP32_TOL = 1e-4
+
+
+def run(ctx, precision="f32"):
+    out = PixelBuffer.zeros(ctx.panel.dims, precision)
+    nanobragg_spots(ctx, out)
+    return out
+
+
+def dims(case):
+    return (int(case["panel"][0]), int(case["panel"][1]))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp64_path_matches_reference(gpu, name):
+    case = parity.load(name)
+    got = run(parity.context(case, "fp64"), "f64").data
+    m = parity.metrics(got, case["ref_f64"], dims(case))
+    assert m["total"] < FP64_TOL and m["spot"] < FP64_TOL, m
+    assert m["pix_abs_over_max"] < FP64_TOL, m
+    # the drop-in f32 store matches the reference's store to the last ulp
+    f32 = run(parity.context(case, "fp64"), "f32").data
+    rel = np.abs(f32.astype(np.float64) - case["ref_f32"]) / np.maximum(np.abs(case["ref_f32"]), 1e-300)
+    assert rel.max() <= 2.0 ** -23, rel.max()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp32_path_matches_reference(gpu, name):
+    case = parity.load(name)
+    got = run(parity.context(case, "fp32"), "f32").data
+    m = parity.metrics(got, case["ref_f64"], dims(case))
+    assert m["total"] < FP32_TOL and m["spot"] < FP32_TOL, m
+
+
+# ---- the reference's own kernel tests, pointed at this implementation (test_kernels.py:99-246) ----
+
+def small_panel():
+    return DetectorPanel(4, 4, 100e-6, 0.1, (1.5, 1.5))
+
+
+def make(**kw):
+    from paper_2205_07976_b200 import CrystalModel, MosaicDomainSet, Orientation, StructureFactorTable, UnitCell
+
+    return CrystalModel(UnitCell(100, 100, 100, 90, 90, 90), kw.get("orientation", Orientation()),
+                        kw.get("n_cells", (5, 5, 5)), kw.get("mosaic", MosaicDomainSet(np.eye(3)[None])),
+                        StructureFactorTable(kw.get("entries", {}), kw.get("default_f", 100.0)))
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_unit_crystal_is_thomson_image(gpu, compute):
+    beam = BeamSpectrum(samples=((1.0, 1.0),), fluence=1e24)
+    ctx = SpotsContext(make(n_cells=(1, 1, 1)), small_panel(), beam, compute=compute)
+    img = run(ctx).as_image()
+    for s in range(4):
+        for f in range(4):
+            pos = pixel_lab_position(small_panel(), s, f, 0.5, 0.5)
+            assert img[s, f] == pytest.approx(R_E_SQR * 1e24 * 100.0 ** 2 * solid_angle(small_panel(), pos),
+                                              rel=1e-6)
+
+
+def test_zero_fluence(gpu):
+    ctx = SpotsContext(make(), small_panel(), BeamSpectrum(samples=((1.0, 1.0),), fluence=0.0))
+    assert np.all(run(ctx).data == 0.0)
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_fluence_linear_default_f_quadratic(gpu, compute):
+    def go(fluence, default_f):
+        ctx = SpotsContext(make(default_f=default_f), small_panel(),
+                           BeamSpectrum(samples=((1.0, 1.0),), fluence=fluence), oversample=2, compute=compute)
+        return run(ctx).data.astype(np.float64)
+
+    base = go(1e20, 50.0)
+    assert np.array_equal(go(2e20, 50.0), 2.0 * base)
+    assert np.array_equal(go(1e20, 100.0), 4.0 * base)
+    assert (np.abs(go(3e20, 50.0) - 3.0 * base) / (3.0 * base)).max() < 1e-7
+
+
+def test_dimension_mismatch(gpu):
+    ctx = SpotsContext(make(), small_panel(), BeamSpectrum(samples=((1.0, 1.0),), fluence=1e24))
+    with pytest.raises(ShapeMismatchError):
+        nanobragg_spots(ctx, PixelBuffer.zeros((3, 4)))
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_numerical_fault_names_lowest_pixel(gpu, compute):
+    ctx = SpotsContext(make(default_f=1e30), small_panel(), BeamSpectrum(samples=((1.0, 1.0),), fluence=1e300),
+                       compute=compute)
+    with pytest.raises(PatternFault) as info:
+        nanobragg_spots(ctx, PixelBuffer.zeros((4, 4)))
+    assert info.value.label == "nanobragg_spots"
+    assert isinstance(info.value.cause, NumericalFault)
+    assert info.value.index == info.value.cause.pixel == 0  # every pixel overflows; lowest is 0
+
+
+def test_fault_index_is_lowest_bad_pixel(gpu):
+    # only the brightest pixels overflow f32: compare with the oracle's lowest bad index
+    case = parity.load("c1_toy")
+    ctx = parity.context(case)
+    desc = describe(ctx)
+    desc.c.fluence = 1e65
+    _, want = oracle.spots(desc, "f32")
+    assert want > 0
+    import dataclasses
+
+    hot = dataclasses.replace(ctx, spectrum=BeamSpectrum(samples=ctx.spectrum.samples, fluence=1e65,
+                                                         polarization_on=True))
+    with pytest.raises(PatternFault) as info:
+        nanobragg_spots(hot, PixelBuffer.zeros(ctx.panel.dims))
+    assert info.value.index == want
+
+
+def test_determinism_and_executor_equivalence(gpu):
+    panel = DetectorPanel(80, 80, 100e-6, 0.12, (39.5, 39.5))
+    beam = BeamSpectrum(samples=((1.0, 0.6), (1.01, 0.4)), fluence=1e24, polarization_on=True)
+    from conftest_helpers import two_domain_mosaic
+
+    ctx = SpotsContext(make(mosaic=two_domain_mosaic()), panel, beam, oversample=2)
+    base = run(ctx).data
+    for n in (1, 2, 4, 8):
+        with Executor.workers(n) as ex:
+            out = PixelBuffer.zeros(panel.dims)
+            nanobragg_spots(ctx, out, executor=ex)
+            assert np.array_equal(out.data, base)
+            assert ex.timing_log and ex.timing_log[-1].label == "nanobragg_spots"
+
+
+# ---- extensions (no reference): GPU vs the CPU oracle ----
+
+def oracle_check(ctx, tol=FP64_TOL):
+    desc = describe(ctx)
+    want, _ = oracle.spots(desc, "f64")
+    got = run(ctx, "f64").data
+    m = parity.metrics(got, want, ctx.panel.dims)
+    assert m["total"] < tol and m["spot"] < tol, m
+    return got, want
+
+
+def roi_ctx(compute="fp64", **kw):
+    panel = synthetic.roi(synthetic.rayonix_panel(), 700, 900, 24, 40)
+    return synthetic.ls49_context(panel=panel, n_channels=8, n_domains=3, compute=compute, **kw)
+
+
+@pytest.mark.parametrize("shape", ["gauss", "round", "tophat"])
+def test_shape_transforms_vs_oracle(gpu, shape):
+    import dataclasses
+
+    ctx = dataclasses.replace(roi_ctx(), shape=shape)
+    oracle_check(ctx)
+    got32 = run(dataclasses.replace(ctx, compute="fp32")).data
+    want, _ = oracle.spots(describe(ctx), "f64")
+    m = parity.metrics(got32, want, ctx.panel.dims)
+    assert m["total"] < FP32_TOL, m
+
+
+def test_thickness_layers_vs_oracle(gpu):
+    import dataclasses
+
+    base = roi_ctx()
+    p = base.panel
+    thick = dataclasses.replace(p, thickness=320e-6, thick_steps=3, attenuation_length=60e-6)
+    oracle_check(dataclasses.replace(base, panel=thick, oversample=2))
+
+
+def test_thin_sensor_is_reference(gpu):
+    import dataclasses
+
+    base = roi_ctx()
+    p1 = dataclasses.replace(base.panel, thick_steps=4)  # thickness 0: steps ignored
+    assert np.array_equal(run(base).data, run(dataclasses.replace(base, panel=p1)).data)
+
+
+def test_phi_scan_vs_oracle_and_identity(gpu):
+    import dataclasses
+
+    base = roi_ctx()
+    ident = dataclasses.replace(base, phi=PhiScan(0.0, 0.0, 1))
+    assert np.array_equal(run(base).data, run(ident).data)
+    oracle_check(dataclasses.replace(base, phi=PhiScan(10.0, 0.3, 3, (0.0, 1.0, 0.0))))
+
+
+def test_multi_panel_equals_single_panels(gpu):
+    import dataclasses
+
+    det = synthetic.jungfrau_detector(n_side=2, size=16, thickness=0.0)
+    ctx = synthetic.ls49_context(panel=det, n_channels=4, n_domains=2, compute="fp64")
+    got, _ = oracle_check(ctx)
+    stacked = got.reshape(4, 16, 16)
+    for i, p in enumerate(det.panels):
+        single = run(dataclasses.replace(ctx, panel=p), "f64").data.reshape(16, 16)
+        assert np.array_equal(single, stacked[i])
+
+
+def test_channel_shards_reduce_to_whole(gpu):
+    from paper_2205_07976_b200 import _native as N
+
+    ctx = roi_ctx()
+    whole = run(ctx, "f64").data
+    plan_all = SpotsPlan(ctx)
+    raw = np.zeros(whole.size)
+    for lo, hi in ((0, 3), (3, 8)):
+        SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=0.0).run(raw, mode=N.OUT_RAW_F64)
+    np.testing.assert_allclose(raw * plan_all.scale, whole, rtol=1e-13, atol=0)
+
+
+def test_plan_runs_into_device_memory(gpu):
+    import torch
+
+    from paper_2205_07976_b200 import _native as N
+
+    ctx = roi_ctx("fp32")
+    plan = SpotsPlan(ctx)
+    dev = torch.zeros(plan.n_pixels, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    plan.run(dev.data_ptr(), mode=N.OUT_F32, on_device=True)
+    host = np.zeros(plan.n_pixels, dtype=np.float32)
+    plan.run(host)
+    assert np.array_equal(dev.cpu().numpy(), host)
+    assert plan.kernel_ms > 0
+
+
+def test_add_array_upcast_semantics(gpu):
+    lhs = PixelBuffer((1, 3), "f64", [0.0, 1.0, 2.0])
+    rhs = PixelBuffer((1, 3), "f32", [0.1, 0.5, 0.25])
+    add_array(lhs, rhs)
+    assert lhs.data.tolist() == [0.10000000149011612, 1.5, 2.25]
+
+
+def test_poisson_noise_bit_exact_with_host_twin(gpu):
+    rng = np.random.default_rng(11)
+    mean = np.concatenate([rng.uniform(0, 12, 50000), rng.uniform(12, 1e4, 50000), [0.0, 1e7]])
+    for prec in ("f64", "f32"):
+        buf = PixelBuffer((1, mean.size), prec, mean)
+        dev = add_noise(buf, seed=1234, image=7).data
+        host = oracle.poisson(buf.data, 1234, 7)
+        assert np.array_equal(dev, host), prec
+    # statistics sanity: mean and variance of a constant field
+    flat = PixelBuffer((1, 200000), "f64", np.full(200000, 37.5))
+    draws = add_noise(flat, seed=9).data
+    assert abs(draws.mean() - 37.5) < 0.1 and abs(draws.var() - 37.5) < 1.0

@@ -1,0 +1,96 @@
+"""The CPU oracle (oracle/) is pinned against the reference's own outputs and known answers (CPU-only)."""
+import math
+
+import numpy as np
+import pytest
+
+import parity
+from oracle import oracle
+from paper_2205_07976_b200 import (
+    CrystalModel,
+    MosaicDomainSet,
+    Orientation,
+    StructureFactorTable,
+    UnitCell,
+    describe,
+    lattice_transform,
+    sincg,
+)
+
+CASES = ["thomson", "scalar_match", "triclinic_pol_2wl", "pipeline_spots", "c1_toy", "tilted", "ls49_centre",
+         "ls49_edge"]
+
+
+def crystal(n_cells=(5, 5, 5)):
+    return CrystalModel(UnitCell(100, 100, 100, 90, 90, 90), Orientation(), n_cells,
+                        MosaicDomainSet(np.eye(3)[None]), StructureFactorTable({}, 100.0))
+
+
+# known-answer values frozen in the reference tests (test_kernels.py:40,64-90)
+def test_sincg_golden():
+    assert sincg(0.0, 5) == 5.0
+    assert sincg(math.pi / 2, 2) == pytest.approx(0.0, abs=1e-15)
+    assert sincg(0.3, 4) == pytest.approx(3.153892914792541, rel=1e-15)
+
+
+def test_lattice_transform_golden():
+    assert abs(lattice_transform(crystal((5, 5, 5)), 2.0, -3.0, 1.0)) == 125.0
+    assert abs(lattice_transform(crystal((3, 4, 7)), 1.0, 0.0, -2.0)) == 84.0
+    assert abs(lattice_transform(crystal((5, 1, 1)), 0.2, 0.0, 0.0)) < 1e-9
+    assert lattice_transform(crystal((4, 1, 1)), 0.3, 0.0, 0.0) == pytest.approx(-0.7265425280053609, rel=1e-14)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_matches_reference_fixture(name):
+    case = parity.load(name)
+    desc = describe(parity.context(case))
+    f64, bad = oracle.spots(desc, "f64")
+    assert bad == -1
+    ref = case["ref_f64"]
+    m = parity.metrics(f64, ref, (int(case["panel"][0]), int(case["panel"][1])))
+    assert m["total"] < 1e-12, m
+    assert m["spot"] < 1e-11, m
+    assert m["pix_abs_over_max"] < 1e-11, m
+    f32, _ = oracle.spots(desc, "f32")
+    same = np.mean(f32 == case["ref_f32"])
+    assert same > 0.99, same
+    ulp = np.abs(f32.astype(np.float64) - case["ref_f32"]) / np.maximum(np.abs(case["ref_f32"]), 1e-300)
+    assert ulp.max() <= 2.0 ** -23
+
+
+def test_oracle_scaling_laws_exact():
+    case = parity.load("scalar_match")
+    base = describe(parity.context(case))
+    img, _ = oracle.spots(base, "f32")
+    desc2 = describe(parity.context(case))
+    desc2.c.fluence = base.c.fluence * 2
+    img2, _ = oracle.spots(desc2, "f32")
+    assert np.array_equal(img2, 2 * img)
+
+
+def test_oracle_channel_shards_sum_to_whole():
+    case = parity.load("pipeline_spots")
+    whole = describe(parity.context(case))
+    raw_whole, _ = oracle.spots(whole, "raw")
+    acc = np.zeros_like(raw_whole)
+    for lo, hi in ((0, 1), (1, 2)):
+        part = describe(parity.context(case), src_begin=lo, src_end=hi)
+        oracle.spots(part, "raw", out=acc)
+    np.testing.assert_allclose(acc, raw_whole, rtol=1e-15, atol=0)
+
+
+def test_oracle_threads_bitwise_invariant():
+    case = parity.load("c1_toy")
+    desc = describe(parity.context(case))
+    a, _ = oracle.spots(desc, "f64", nthreads=1)
+    b, _ = oracle.spots(desc, "f64", nthreads=7)
+    assert np.array_equal(a, b)
+
+
+def test_oracle_fault_pixel():
+    case = parity.load("thomson")
+    desc = describe(parity.context(case))
+    desc.c.fluence = 1e300
+    desc.c.default_f = 1e30
+    _, bad = oracle.spots(desc, "f32")
+    assert bad == 0

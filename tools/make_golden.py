@@ -1,0 +1,173 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation.
+
+Run here (where /root/reference exists):  python tools/make_golden.py
+The GPU box never runs this; it only reads the committed fixtures.
+
+Each fixture stores the exact inputs as plain arrays (cell, orientation,
+mosaic rotations, Fhkl entries, panel, spectrum, oversample) plus
+  ref_f32 : xtrace.kernels.nanobragg_spots output (FP64 math, f32 store)
+  ref_f64 : the same code with the f32 cast intercepted ("oracle64",
+            SURVEY §8 C1): the FP64 values before the store
+Checks done while generating: f32(ref_f64) == ref_f32 bit for bit, and the
+package's own mosaic generator reproduces the reference's matrices exactly.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+import types
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import xtrace.kernels as xk  # noqa: E402
+import xtrace.model as xm  # noqa: E402
+
+from paper_2205_07976_b200 import model as mm  # noqa: E402
+from paper_2205_07976_b200 import synthetic as syn  # noqa: E402
+
+OUT = ROOT / "tests" / "golden"
+
+
+def rotation_about(axis, angle_deg):
+    axis = np.asarray(axis, dtype=float)
+    axis = axis / np.linalg.norm(axis)
+    ang = np.radians(angle_deg)
+    ax, ay, az = axis
+    k = np.array([[0, -az, ay], [az, 0, -ax], [-ay, ax, 0]])
+    return np.eye(3) + np.sin(ang) * k + (1 - np.cos(ang)) * (k @ k)
+
+
+def run_reference(case):
+    """(ref_f32, ref_f64) from xtrace for one case dict of arrays."""
+    cell = xm.UnitCell(*case["cell"])
+    crystal = xm.CrystalModel(
+        cell=cell,
+        orientation=xm.Orientation(case["orientation"]),
+        n_cells=tuple(int(x) for x in case["n_cells"]),
+        mosaic=xm.MosaicDomainSet(case["mosaic"]),
+        sf_table=xm.StructureFactorTable(
+            {tuple(int(v) for v in h): float(a) for h, a in zip(case["hkl"], case["amp"])},
+            default_f=float(case["default_f"])),
+    )
+    p = case["panel"]
+    panel = xm.DetectorPanel(int(p[0]), int(p[1]), float(p[2]), float(p[3]), (float(p[4]), float(p[5])),
+                             fast_axis=tuple(case["fast_axis"]), slow_axis=tuple(case["slow_axis"]))
+    beam = xm.BeamSpectrum(samples=tuple(map(tuple, case["samples"])), fluence=float(case["fluence"]),
+                           polarization_on=bool(case["pol"]), beam_direction=tuple(case["beam_dir"]))
+    ctx = xk.SpotsContext(crystal, panel, beam, oversample=int(case["oversample"]))
+    out32 = xk.PixelBuffer.zeros(panel.dims)
+    xk.nanobragg_spots(ctx, out32)
+
+    # oracle64: same code, cast intercepted (kernels.py:271-273)
+    cap = np.zeros(panel.n_pixels)
+    shim = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np) if not k.startswith("__")})
+    shim.float32 = np.float64
+    real_np, real_store = xk.np, xk._store_checked
+
+    def store(out_slice, values, lo):
+        cap[lo:lo + len(values)] = values
+        real_store(out_slice, values, lo)
+
+    xk.np, xk._store_checked = shim, store
+    try:
+        out64 = xk.PixelBuffer.zeros(panel.dims)
+        xk.nanobragg_spots(ctx, out64)
+    finally:
+        xk.np, xk._store_checked = real_np, real_store
+    assert np.array_equal(cap.astype(np.float32), out32.data), "f32(oracle64) != reference store"
+    return out32.data.copy(), cap
+
+
+def base_case(**kw):
+    c = dict(cell=(100.0, 100.0, 100.0, 90.0, 90.0, 90.0), orientation=np.eye(3), n_cells=(5, 5, 5),
+             mosaic=np.eye(3)[None], hkl=np.zeros((0, 3), np.int32), amp=np.zeros(0), default_f=100.0,
+             panel=(4, 4, 100e-6, 0.1, 1.5, 1.5), fast_axis=(1.0, 0.0, 0.0), slow_axis=(0.0, 1.0, 0.0),
+             samples=np.array([[1.0, 1.0]]), fluence=1e24, pol=False, beam_dir=(0.0, 0.0, 1.0), oversample=1)
+    c.update(kw)
+    return c
+
+
+def two_domain():
+    return np.stack([rotation_about([1, 0, 0], 0.02), rotation_about([0, 1, 1], -0.03)])
+
+
+def entries(d):
+    hkl = np.array(list(d.keys()), dtype=np.int32).reshape(-1, 3)
+    amp = np.array(list(d.values()), dtype=float)
+    return hkl, amp
+
+
+def ls49_case(r0, c0, rows, cols, n_channels, n_domains, seed=syn.SEED, compute_note=""):
+    crystal = syn.ls49_crystal(seed, n_domains)
+    # the package's mosaic draw must equal the reference's, bit for bit
+    ref_mos = xm.generate_mosaic_rotations(seed, 0.05, n_domains).rotations
+    assert np.array_equal(ref_mos, crystal.mosaic.rotations), "mosaic generator differs from the reference"
+    spec = syn.ls49_spectrum(n_channels, 7070.0, 1.0, seed)
+    full = syn.rayonix_panel()
+    hkl, amp = crystal.sf_table.arrays()
+    return base_case(cell=syn.LS49_CELL, orientation=crystal.orientation.u, n_cells=syn.LS49_NCELLS,
+                     mosaic=crystal.mosaic.rotations, hkl=hkl, amp=amp, default_f=0.0,
+                     panel=(rows, cols, full.pixel_size, full.distance, full.beam_center[0] - r0,
+                            full.beam_center[1] - c0),
+                     samples=np.array(spec.samples), fluence=spec.fluence, pol=True)
+
+
+CASES = {
+    # test_kernels.py:100-111 -- unit crystal is the Thomson image
+    "thomson": base_case(n_cells=(1, 1, 1)),
+    # test_kernels.py:120-145
+    "scalar_match": base_case(mosaic=two_domain(), oversample=2,
+                              **dict(zip(("hkl", "amp"), entries({(0, 0, 0): 300.0, (1, 0, 0): 50.0,
+                                                                  (0, 1, 0): 80.0})))),
+    # test_kernels.py:147-175
+    "triclinic_pol_2wl": base_case(cell=(60, 70, 80, 85, 92, 103), orientation=rotation_about([0.2, 1.0, -0.4], 13.0),
+                                   n_cells=(4, 3, 6), mosaic=two_domain(), default_f=20.0, oversample=3,
+                                   panel=(5, 3, 150e-6, 0.08, 2.0, 1.25),
+                                   samples=np.array([[1.0, 0.75], [1.02, 0.25]]), fluence=5e23, pol=True,
+                                   **dict(zip(("hkl", "amp"), entries({(1, 1, 1): 40.0})))),
+    # test_kernels.py:439-471 (spot part of the pipeline)
+    "pipeline_spots": base_case(mosaic=two_domain(), oversample=2, samples=np.array([[1.0, 0.6], [1.05, 0.4]]),
+                                pol=True, **dict(zip(("hkl", "amp"), entries({(1, 0, 0): 250.0})))),
+    # C1 toy (test_acceptance.py:52-65 shape at 256^2, bc on a pixel centre -> limit branch)
+    "c1_toy": base_case(panel=(256, 256, 100e-6, 0.1, 127.5, 127.5), pol=True,
+                        **dict(zip(("hkl", "amp"), entries({(1, 0, 0): 250.0})))),
+    # tilted panel axes + off-axis beam
+    "tilted": base_case(cell=(50, 60, 70, 90, 90, 90), orientation=rotation_about([1, 2, 3], 40.0),
+                        n_cells=(7, 8, 9), panel=(24, 20, 172e-6, 0.09, 11.3, 8.7),
+                        fast_axis=tuple(rotation_about([0, 1, 0], 10.0) @ [1.0, 0, 0]),
+                        slow_axis=tuple(rotation_about([0, 1, 0], 10.0) @ [0, 1.0, 0]),
+                        beam_dir=tuple(rotation_about([1, 0, 0], 3.0) @ [0, 0, 1.0]),
+                        samples=np.array([[1.3, 0.2], [1.31, 0.5], [1.32, 0.3]]), pol=True, default_f=10.0,
+                        **dict(zip(("hkl", "amp"), entries({(1, 1, 0): 30.0, (0, 1, 1): 70.0, (2, 0, 1): 5.0})))),
+    # LS49-shape ROIs: one through the beam centre (q = 0 pixel, F000), one at high resolution
+    "ls49_centre": ls49_case(1888, 1888, 64, 64, 20, 10),
+    "ls49_edge": ls49_case(96, 160, 48, 96, 100, 50),
+}
+
+
+def main(names):
+    OUT.mkdir(parents=True, exist_ok=True)
+    meta = {}
+    for name in names or CASES:
+        case = CASES[name]
+        t0 = time.perf_counter()
+        f32, f64 = run_reference(case)
+        dt = time.perf_counter() - t0
+        arrays = {k: np.asarray(v) for k, v in case.items()}
+        np.savez_compressed(OUT / f"{name}.npz", ref_f32=f32, ref_f64=f64, **arrays)
+        meta[name] = {"pixels": int(f32.size), "ref_seconds": round(dt, 2), "total_f64": float(f64.sum()),
+                      "max_f64": float(f64.max())}
+        print(name, meta[name], flush=True)
+    old = json.loads((OUT / "index.json").read_text()) if (OUT / "index.json").exists() else {}
+    old.update(meta)
+    (OUT / "index.json").write_text(json.dumps(old, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
