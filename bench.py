@@ -1,0 +1,416 @@
+"""Benchmark: LS49-shape spot images (BASELINE.json configs[1], C2) on 1..8 B200s.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, image-sharded)
+
+One step = one full C2 image per GPU (3840 x 3840 pixels, 100 energy channels,
+50 mosaic domains, oversample 1: 7.3728e10 pixel x source x mosaic steps),
+each image with its own orientation / mosaic / weight seed (C3 sharding: no
+collective).  `value` is whole-job images/s with every input resident in HBM
+(device time, CUDA events, max over ranks); `e2e` is the same metric through
+the drop-in nanobragg_spots() call with host buffers (descriptor upload and
+image download inside the timed region).  Prints ONE JSON line on rank 0.
+
+--impl reference times the reference's own CPU implementation (xtrace from
+baseline/_ref, NumPy FP64, one forked process per host core on row stripes,
+SURVEY §8 D1) on a bounded sample of the same workload; the C oracle port is
+used if baseline/_ref is absent.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "images/s and Gsteps/s (pixel×source×mosaic×subpixel) at 1/2/4/8 B200"
+WORKLOAD = "C2 LS49-shape image: 3840x3840 Rayonix-like, 100 energy channels, 50 mosaic domains, oversample 1"
+STEP_INSTR = 126  # FP-pipe instructions per step, SURVEY §8 D1 (FMA = 1)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--compute", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--size", type=int, default=3840)
+    ap.add_argument("--channels", type=int, default=100)
+    ap.add_argument("--domains", type=int, default=50)
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / fp64 / cpu-baseline legs")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
+                 str(self.device), "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        mhz, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                mhz.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [m for m in mhz if m > 300] or mhz
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    world, rank, local = dist_env()
+    os.environ["NBX_DEVICE"] = str(local)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from oracle import oracle  # cpu_baseline leg only (the checker, never the thing measured)
+    from paper_2205_07976_b200 import PixelBuffer, SpotsPlan, nanobragg_spots, synthetic
+    from paper_2205_07976_b200 import _native as N
+
+    cx = N.context(local)
+    # one non-default stream shared by torch (flush, events) and the library (kernels, copies)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    cx.lib.nbx_ctx_set_stream(cx.handle, N.C.c_void_p(stream.cuda_stream))
+
+    size = args.size
+    r0 = (3840 - size) // 2
+    panel = synthetic.rayonix_panel() if size == 3840 else synthetic.roi(synthetic.rayonix_panel(), r0, r0, size, size)
+
+    def ctx_for(i, compute):
+        return synthetic.ls49_context(synthetic.SEED + 100003 * rank + i, n_channels=args.channels,
+                                      n_domains=args.domains, panel=panel, compute=compute)
+
+    n_img = args.warmup + args.steps
+    plans = [SpotsPlan(ctx_for(i, args.compute), device=local) for i in range(n_img)]
+    steps_per_image = plans[0].steps
+    out = torch.empty(plans[0].n_pixels, dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        flush.zero_()
+        plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+
+    # roofline denominator: live FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32 figure)
+    peak = N.C.c_double(0.0)
+    cx.lib.nbx_probe_fma_peak(cx.handle, 1 if args.compute == "fp64" else 0, N.C.byref(peak))
+
+    kernel_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for i in range(args.warmup, n_img):
+            flush.zero_()
+            plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            kernel_ms.append(plans[i].kernel_ms)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    total_images = world * args.steps
+    value = total_images / (elapsed / 1e3)
+    gsteps = total_images * steps_per_image / (elapsed / 1e3) / 1e9
+    mean_kernel = statistics.fmean(kernel_ms)
+    achieved = STEP_INSTR * 2.0 * steps_per_image / (mean_kernel / 1e3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"spots_{args.compute}", {}).get("dram_bytes_per_launch")
+        except (ValueError, AttributeError):
+            traffic = None
+    result = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.compute == "fp32" else "f64",
+        "data": "synthetic (seeded LS49-shape crystal, Wilson Fhkl to 1.6 A, random orientation per image)",
+        "config": {"workload": WORKLOAD if size == 3840 else f"{WORKLOAD} (ROI {size}x{size})",
+                   "images_per_gpu_per_step": 1, "global_batch": world, "steps_per_image": steps_per_image,
+                   "compute": args.compute, "parallelism": f"image-sharded x{world} (no collective)",
+                   "l2": "256 MB buffer written between timed images (L2 flushed); Fhkl grid L2-resident by design"},
+        "gsteps_per_s": gsteps,
+        "kernel_ms_mean": mean_kernel,
+        "gpu_launches": args.steps,  # one spot kernel per image; the flush is torch's fill, not ours
+        "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
+                     "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
+                     "traffic": traffic,
+                     "basis": f"{STEP_INSTR} FP-pipe instr/step x 2 FLOP x steps / mean spot-kernel time; "
+                              "peak = live FMA probe (nbx_probe_fma_peak) on this GPU"},
+        "clocks": clocks.summary(),
+    }
+
+    if rank == 0 and not args.no_extras:
+        # e2e: drop-in API, host PixelBuffer, everything inside the timed region
+        from paper_2205_07976_b200.kernels import SpotsContext
+
+        e2e_steps = max(1, min(args.steps, 3))
+        ctxs = [ctx_for(1000 + i, args.compute) for i in range(e2e_steps + 1)]
+        img = PixelBuffer.zeros(panel.dims, "f32")
+        nanobragg_spots(ctxs[0], img)  # warm (host tables, context)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for c in ctxs[1:]:
+            nanobragg_spots(c, img)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = ev0.elapsed_time(ev1) / e2e_steps
+        info = plans[0].info
+        h2d = int(info.table_cells) * (4 if args.compute == "fp32" else 8) + args.channels * 16 + \
+            args.domains * 72 + 160
+        result["e2e"] = {"value": 1e3 / e2e_ms, "unit": "images/s", "h2d_bytes_per_step": h2d,
+                         "d2h_bytes_per_step": int(plans[0].n_pixels) * 4 + 8, "ms_per_step": e2e_ms,
+                         "api": "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"}
+
+        # FP64 path on the same workload (the 1e-9 parity path)
+        p64 = SpotsPlan(ctx_for(0, "fp64"), device=local)
+        p64.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+        ms64 = []
+        for _ in range(2):
+            flush.zero_()
+            p64.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            ms64.append(p64.kernel_ms)
+        peak64 = N.C.c_double(0.0)
+        cx.lib.nbx_probe_fma_peak(cx.handle, 1, N.C.byref(peak64))
+        ach64 = STEP_INSTR * 2.0 * p64.steps / (statistics.fmean(ms64) / 1e3) / 1e12
+        result["fp64_path"] = {"kernel_ms": statistics.fmean(ms64),
+                               "gsteps_per_s": p64.steps / statistics.fmean(ms64) / 1e6,
+                               "roofline": {"bound": "fp64_pipe", "achieved": ach64, "peak": peak64.value,
+                                            "unit": "TFLOP/s", "frac": ach64 / peak64.value if peak64.value else None}}
+        p64.close()
+
+        if world == 1:
+            result["cpu_baseline"] = cpu_baseline_port(ctx_for(0, "fp64"), panel, steps_per_image, oracle)
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    for p in plans:
+        p.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_port(ctx, panel, steps_per_image, oracle):
+    """The C oracle (FP64 scalar restatement) on all host cores over a 16-row ROI of the image."""
+    from paper_2205_07976_b200 import describe, synthetic
+
+    rows = 16
+    r0 = panel.slow_pixels // 2 - rows // 2
+    import dataclasses
+
+    sub = dataclasses.replace(ctx, panel=synthetic.roi(panel, r0, 0, rows, panel.fast_pixels))
+    desc = describe(sub)
+    cores = host_cores()
+    t0 = time.perf_counter()
+    oracle.spots(desc, "f32", nthreads=cores)
+    dt = time.perf_counter() - t0
+    sample_steps = rows * panel.fast_pixels * steps_per_image // panel.n_pixels
+    sps = sample_steps / dt
+    return {"value": sps / steps_per_image, "unit": "images/s", "cores": cores, "kind": "port",
+            "gsteps_per_s": sps / 1e9, "seconds": dt, "cpu": cpu_model(),
+            "sample": f"rows {r0}-{r0 + rows - 1} x {panel.fast_pixels} px x all sources x all domains "
+                      f"({sample_steps:.3g} steps) of the same image, oracle/nbx_oracle.c FP64, {cores} threads"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def _xtrace_available():
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "xtrace" / "kernels.py").exists():
+        sys.path.insert(0, str(ref))
+        return True
+    return False
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference; the others exit without work
+    from paper_2205_07976_b200 import synthetic
+
+    size = args.size
+    panel = synthetic.rayonix_panel() if size == 3840 else synthetic.roi(
+        synthetic.rayonix_panel(), (3840 - size) // 2, (3840 - size) // 2, size, size)
+    ctx = synthetic.ls49_context(synthetic.SEED, n_channels=args.channels, n_domains=args.domains, panel=panel,
+                                 compute="fp64")
+    steps_per_image = panel.n_pixels * args.channels * args.domains
+    cores = host_cores()
+    rows_per_step = cores  # one full-width row per forked process per step
+    kind = "reference" if _xtrace_available() else "port"
+    step_fn = _reference_step_xtrace(ctx, panel, cores) if kind == "reference" else _reference_step_port(ctx, panel, cores)
+    row0 = panel.slow_pixels // 2 - rows_per_step // 2
+    for i in range(args.warmup):
+        step_fn(row0 + i % 4, rows_per_step)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        step_fn(row0, rows_per_step)
+        times.append(time.perf_counter() - t0)
+    sample_steps = rows_per_step * panel.fast_pixels * args.channels * args.domains
+    sec = sum(times)
+    sps = sample_steps * args.steps / sec
+    value = sps / steps_per_image
+    sample = (f"{rows_per_step} full-width rows ({rows_per_step}x{panel.fast_pixels} px) x {args.channels} sources x "
+              f"{args.domains} domains = {sample_steps:.3g} steps per step")
+    impl_desc = ("xtrace.kernels.nanobragg_spots (baseline/_ref, unmodified, NumPy FP64) in one forked process "
+                 "per core on row-stripe sub-panels" if kind == "reference" else
+                 "oracle/nbx_oracle.c FP64 restatement, one thread per core")
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded LS49-shape workload)",
+        "config": {"workload": WORKLOAD, "steps_per_image": steps_per_image, "impl": impl_desc},
+        "impl": "reference", "gsteps_per_s": sps / 1e9,
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind, "sample": sample,
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _reference_step_xtrace(ctx, panel, cores):
+    import multiprocessing as mp
+
+    import numpy as np
+    import xtrace.kernels as xk
+    import xtrace.model as xm
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    c = ctx.crystal
+    hkl, amp = c.sf_table.arrays()
+    xcrystal = xm.CrystalModel(
+        cell=xm.UnitCell(c.cell.a, c.cell.b, c.cell.c, c.cell.alpha, c.cell.beta, c.cell.gamma),
+        orientation=xm.Orientation(c.orientation.u), n_cells=c.n_cells,
+        mosaic=xm.MosaicDomainSet(np.array(c.mosaic.rotations)),
+        sf_table=xm.StructureFactorTable({tuple(map(int, h)): float(a) for h, a in zip(hkl, amp)},
+                                         default_f=c.sf_table.default_f))
+    s = ctx.spectrum
+    xbeam = xm.BeamSpectrum(samples=s.samples, fluence=s.fluence, polarization_on=s.polarization_on,
+                            beam_direction=s.beam_direction)
+    fork = mp.get_context("fork")
+
+    def one_row(r):
+        p = xm.DetectorPanel(1, panel.fast_pixels, panel.pixel_size, panel.distance,
+                             (panel.beam_center[0] - r, panel.beam_center[1]))
+        xctx = xk.SpotsContext(xcrystal, p, xbeam, oversample=ctx.oversample)
+        out = xk.PixelBuffer.zeros(p.dims)
+        xk.nanobragg_spots(xctx, out)
+        os._exit(0)
+
+    def step(r0, rows):
+        procs = [fork.Process(target=one_row, args=(r0 + i,)) for i in range(rows)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join()
+
+    return step
+
+
+def _reference_step_port(ctx, panel, cores):
+    from oracle import oracle
+    from paper_2205_07976_b200 import describe, synthetic
+
+    import dataclasses
+
+    def step(r0, rows):
+        sub = dataclasses.replace(ctx, panel=synthetic.roi(panel, r0, 0, rows, panel.fast_pixels))
+        oracle.spots(describe(sub), "f32", nthreads=cores)
+
+    return step
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

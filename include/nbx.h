@@ -178,6 +178,12 @@ int nbx_add_noise(void* ctx, const void* mean, void* out, int64_t n, int dtype,
 int nbx_poisson_host(const void* mean, void* out, int64_t n, int dtype,
                      uint64_t seed, uint64_t image);
 
+/* Measurement utility (roofline denominator; MEASURED_PEAKS.json has no FP32/FP64
+ * figure): dense FMA throughput of this GPU in TFLOP/s (FMA = 2 FLOP), fp64 = 0
+ * for FP32 FFMA, 1 for FP64 DFMA.  Runs ~50-100 ms of independent FMA chains on
+ * every SM. */
+int nbx_probe_fma_peak(void* ctx, int fp64, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ EXPORTS = (
     "nbx_version", "nbx_ctx_create", "nbx_ctx_destroy", "nbx_last_error", "nbx_ctx_set_stream",
     "nbx_ctx_synchronize", "nbx_output_pixels", "nbx_spots", "nbx_spots_batch", "nbx_plan_create",
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
-    "nbx_add_array", "nbx_add_noise", "nbx_poisson_host",
+    "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak",
 )
 
 
@@ -97,6 +97,7 @@ def load() -> C.CDLL:
             "nbx_add_array": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int]),
             "nbx_add_noise": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, C.c_uint64, C.c_uint64, C.c_int]),
             "nbx_poisson_host": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_uint64, C.c_uint64]),
+            "nbx_probe_fma_peak": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -15,9 +15,11 @@
 //   * The reference's limit branch (|sin x| < 1e-12 -> N cos(Nx)/cos(x)) is the
 //     t -> 0 limit of the same ratio; biasing |t| by a tiny constant makes the
 //     ratio evaluate to N there with no branch.
-//   * FP32 path: the fractional Miller index is split exactly (double-float
-//     product with FMA), so t carries ~3e-8 absolute error even for |h| ~ 50;
-//     the sin polynomials and the ratio then run in FP32.
+//   * FP32 path: the phase is anchored per (pixel, domain, channel chunk) in
+//     FP64 (h0 = S / lambda0 = n0 + f0), and per channel only the small offset
+//     x = f0 + S (1/lambda_w - 1/lambda0) is formed in FP32 (|x| <= 2 by the
+//     host's chunking), so t carries ~5e-8 absolute error even for |h| ~ 50.
+//     All roundings are magic-number adds on the FMA pipe (no FRND/XU).
 #pragma once
 
 #include <cstdint>
@@ -26,29 +28,49 @@
 namespace nbx {
 
 // ---------------------------------------------------------------------------
-// Q(s) = sin(pi sqrt(s)) / (pi sqrt(s)), s in [0, 0.2704] (|x| <= 0.52).
-// Relative-minimax fits made by tools/fit_sinpi.py (mpmath, 60 digits).
-// FP32: degree 4, max rel err 9.1e-9.  FP64: degree 7, max rel err 2.9e-16.
+// Q(s) = sin(pi sqrt(s)) / (pi sqrt(s)), s in [0, 0.2704] (|x| <= 0.52), Q(0) = 1.
+// Relative-minimax fits made by tools/fit_sinpi.py (mpmath, 60 digits):
+//   FP32 degree 3: max rel err 1.5e-6   (the ratio error stays < 1e-5 per step)
+//   FP32 degree 4: max rel err 9.1e-9
+//   FP64 degree 6: max rel err 1.2e-13  (1e4 below the 1e-9 parity bar)
+//   FP64 degree 7: max rel err 2.9e-16
 // ---------------------------------------------------------------------------
+template <int DEG>
 __device__ __forceinline__ float q_sinpi_f32(float s) {
-    float q = 0.02460929274903431744f;
-    q = __fmaf_rn(q, s, -0.1903951449679496331f);
-    q = __fmaf_rn(q, s, 0.8117093632737977162f);
-    q = __fmaf_rn(q, s, -1.644933097370079417f);
-    q = __fmaf_rn(q, s, 1.0f);
-    return q;
+    if constexpr (DEG == 3) {
+        float q = -0.1772475662559543266f;
+        q = __fmaf_rn(q, s, 0.8095661799590536796f);
+        q = __fmaf_rn(q, s, -1.644831841650291668f);
+        return __fmaf_rn(q, s, 1.0f);
+    } else {
+        float q = 0.02460929274903431744f;
+        q = __fmaf_rn(q, s, -0.1903951449679496331f);
+        q = __fmaf_rn(q, s, 0.8117093632737977162f);
+        q = __fmaf_rn(q, s, -1.644933097370079417f);
+        return __fmaf_rn(q, s, 1.0f);
+    }
 }
 
+template <int DEG>
 __device__ __forceinline__ double q_sinpi_f64(double s) {
-    double q = -0.000006705758238410946132099385;
-    q = __fma_rn(q, s, 0.000148310321408001520683082);
-    q = __fma_rn(q, s, -0.002346053946710248122556649);
-    q = __fma_rn(q, s, 0.02614784439741657402822952);
-    q = __fma_rn(q, s, -0.1907518238899222190335658);
-    q = __fma_rn(q, s, 0.8117424252758336467922741);
-    q = __fma_rn(q, s, -1.644934066848143329530488);
-    q = __fma_rn(q, s, 1.0);
-    return q;
+    if constexpr (DEG == 6) {
+        double q = 0.0001419369313558917659014215;
+        q = __fma_rn(q, s, -0.002343678327814821972139302);
+        q = __fma_rn(q, s, 0.02614740711391976615878763);
+        q = __fma_rn(q, s, -0.1907517829843114062130668);
+        q = __fma_rn(q, s, 0.8117424235039948673634413);
+        q = __fma_rn(q, s, -1.64493406682232519873061);
+        return __fma_rn(q, s, 1.0);
+    } else {
+        double q = -0.000006705758238410946132099385;
+        q = __fma_rn(q, s, 0.000148310321408001520683082);
+        q = __fma_rn(q, s, -0.002346053946710248122556649);
+        q = __fma_rn(q, s, 0.02614784439741657402822952);
+        q = __fma_rn(q, s, -0.1907518238899222190335658);
+        q = __fma_rn(q, s, 0.8117424252758336467922741);
+        q = __fma_rn(q, s, -1.644934066848143329530488);
+        return __fma_rn(q, s, 1.0);
+    }
 }
 
 __device__ __forceinline__ float rcp_approx_f32(float x) {
@@ -57,14 +79,16 @@ __device__ __forceinline__ float rcp_approx_f32(float x) {
     return y;
 }
 
+// MUFU seed refined by Newton steps (each squares the relative error).
+template <int NR>
 __device__ __forceinline__ double rcp_f64(double x) {
-    // MUFU seed + two Newton steps: full double precision for normal x.
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
-    e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const double e = __fma_rn(-x, y, 1.0);
+        y = __fma_rn(y, e, y);
+    }
     return y;
 }
 
@@ -81,13 +105,18 @@ __device__ __forceinline__ double round_half_away(double x) {
 // three biased terms stays a normal number in the path's precision.
 constexpr float kTBiasF32 = 1e-12f;
 constexpr double kTBiasF64 = 1e-30;
+// 1.5 * 2^23: x + kMagicF32 - kMagicF32 == rint(x) for |x| < 2^22, on the FMA pipe.
+constexpr float kMagicF32 = 12582912.0f;
 
-// One axis of the FP64 grating: returns numerator r*Q(r^2) and denominator
-// t*Q(t^2) of |sin(N pi h)/sin(pi h)|, plus the rounded index and t.
+// ---------------------------------------------------------------------------
+// FP64 axis: numerator r Q(r^2) and denominator t Q(t^2) of |sin(N pi h)/sin(pi h)|,
+// plus the reference-rounded index n and t = h - n.
+// ---------------------------------------------------------------------------
 struct AxisF64 {
     double num, den, n, t;
 };
 
+template <int DEG>
 __device__ __forceinline__ AxisF64 axis_f64(double S, double iv, double N) {
     AxisF64 a;
     const double h = S * iv;                      // kernels.py:257-260 (sa * (1/lambda))
@@ -96,32 +125,33 @@ __device__ __forceinline__ AxisF64 axis_f64(double S, double iv, double N) {
     const double ta = fabs(a.t) + kTBiasF64;
     const double k = rint(N * ta);
     const double r = __fma_rn(N, ta, -k);         // N t - k, one rounding
-    a.num = r * q_sinpi_f64(r * r);
-    a.den = ta * q_sinpi_f64(ta * ta);
+    a.num = r * q_sinpi_f64<DEG>(r * r);
+    a.den = ta * q_sinpi_f64<DEG>(ta * ta);
     return a;
 }
 
+// ---------------------------------------------------------------------------
+// FP32 axis, phase anchored per chunk: x = f0 + S_hi * D where h = n0 + x.
+// m = x + M holds j = rint(x) as M + j (used directly by the index FMA chain).
+// ---------------------------------------------------------------------------
 struct AxisF32 {
-    float num, den, n, t;
+    float num, den, j, m, t;
 };
 
-// S = S_hi + S_lo and 1/lambda = iv_hi + iv_lo are double-float splits of the
-// FP64 values; t = S*iv - rint(S*iv) is formed with one rounding at |t| <= 1/2
-// scale (the FMA absorbs the exact product error), so the phase is FP64-grade.
-__device__ __forceinline__ AxisF32 axis_f32(float S_hi, float S_lo, float iv_hi, float iv_lo,
-                                            float N) {
+// `magic` is kMagicF32 or kMagicF32 + (integer < 2^22): m then carries that
+// integer offset for free (the index chain uses it to fold in the chunk's cell).
+template <int DEG>
+__device__ __forceinline__ AxisF32 axis_f32(float S_hi, float D, float f0, float N, float magic = kMagicF32) {
     AxisF32 a;
-    const float p = S_hi * iv_hi;
-    a.n = rintf(p);
-    float t = __fmaf_rn(S_hi, iv_hi, -a.n);       // (S_hi*iv_hi - n) exactly, rounded once
-    t = __fmaf_rn(S_hi, iv_lo, t);
-    t = __fmaf_rn(S_lo, iv_hi, t);
-    a.t = t;
-    const float ta = fabsf(t) + kTBiasF32;
-    const float k = rintf(N * ta);
+    const float x = __fmaf_rn(S_hi, D, f0);
+    a.m = __fadd_rn(x, magic);
+    a.j = __fsub_rn(a.m, magic);                  // rint(x), exact
+    a.t = __fsub_rn(x, a.j);                      // exact
+    const float ta = fabsf(a.t) + kTBiasF32;
+    const float k = __fsub_rn(__fmaf_rn(N, ta, kMagicF32), kMagicF32);  // rint(N t)
     const float r = __fmaf_rn(N, ta, -k);
-    a.num = r * q_sinpi_f32(r * r);
-    a.den = ta * q_sinpi_f32(ta * ta);
+    a.num = r * q_sinpi_f32<DEG>(r * r);
+    a.den = ta * q_sinpi_f32<DEG>(ta * ta);
     return a;
 }
 

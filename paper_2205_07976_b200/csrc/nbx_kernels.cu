@@ -22,31 +22,45 @@ enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3 };
 
 constexpr int kBlockX = 32;
 constexpr int kBlockY = 8;
-constexpr int kChanChunk = 64;  // FP32 partial sums are flushed to FP64 every 64 channels
+constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
+constexpr int kPolyF64 = 6;  // FP64 Q(s) degree (rel err 1.2e-13)
+constexpr int kNewtonF64 = 1;
 
 // ---------------------------------------------------------------------------
 // Sum over channels of w * F^2 * F_latt^2 for one (pixel, sub-pixel, domain).
+// FP32 path: channels come in chunks with one FP64 phase anchor each; the
+// chunk's F^2 base pointer is biased so that the magic-number float built by
+// the index FMA chain is directly the byte offset / 4.
 // ---------------------------------------------------------------------------
-template <int SHAPE, bool WIDE>
-__device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const float4* __restrict__ sch,
-                                                 double Sa, double Sb, double Sc) {
+template <int SHAPE, bool WIDE, int PDEG>
+__device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const ChunkF32* __restrict__ sck,
+                                                 const float2* __restrict__ sch, double Sa, double Sb,
+                                                 double Sc) {
     const float a_hi = __double2float_rn(Sa), b_hi = __double2float_rn(Sb), c_hi = __double2float_rn(Sc);
-    const float a_lo = __double2float_rn(Sa - (double)a_hi);
-    const float b_lo = __double2float_rn(Sb - (double)b_hi);
-    const float c_lo = __double2float_rn(Sc - (double)c_hi);
     const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
-    const float* __restrict__ tab = static_cast<const float*>(P.table);
     const float sHf = (float)P.sH, sKf = (float)P.sK;
+    const float* tab_biased = static_cast<const float*>(P.table) - (int64_t)0x4B400000;
     double dacc = 0.0;
-    for (int w0 = 0; w0 < P.n_src; w0 += kChanChunk) {
-        const int we = min(P.n_src, w0 + kChanChunk);
+    for (int ci = 0; ci < P.n_chunks; ++ci) {
+        const ChunkF32 ck = sck[ci];
+        // FP64 anchor: h0 = S * iv0 = n0 + f0 per axis
+        const double ha = Sa * ck.iv0, hb = Sb * ck.iv0, hc = Sc * ck.iv0;
+        const int na = __double2int_rn(ha), nb = __double2int_rn(hb), nc = __double2int_rn(hc);
+        const float fa = __double2float_rn(ha - (double)na);
+        const float fb = __double2float_rn(hb - (double)nb);
+        const float fc = __double2float_rn(hc - (double)nc);
+        const int64_t cell0 = (int64_t)(na - P.lo[0]) * P.sH + (int64_t)(nb - P.lo[1]) * P.sK + (nc - P.lo[2]);
+        // !WIDE: the l-axis magic carries cell0, so float_bits(M + cell0 + offset)
+        // - 0x4B400000 is the absolute cell; WIDE: per-chunk base + int offset
+        const float magic_c = WIDE ? kMagicF32 : kMagicF32 + (float)cell0;
+        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : 0);
         float accf = 0.0f;
 #pragma unroll 2
-        for (int w = w0; w < we; ++w) {
-            const float4 c = sch[w];
-            const AxisF32 A = axis_f32(a_hi, a_lo, c.x, c.y, Na);
-            const AxisF32 B = axis_f32(b_hi, b_lo, c.x, c.y, Nb);
-            const AxisF32 C = axis_f32(c_hi, c_lo, c.x, c.y, Nc);
+        for (int w = ck.begin; w < ck.end; ++w) {
+            const float2 c = sch[w];
+            const AxisF32 A = axis_f32<PDEG>(a_hi, c.x, fa, Na);
+            const AxisF32 B = axis_f32<PDEG>(b_hi, c.x, fb, Nb);
+            const AxisF32 C = axis_f32<PDEG>(c_hi, c.x, fc, Nc, magic_c);
             float L2;
             if constexpr (SHAPE == 0) {
                 const float nn = (A.num * B.num) * C.num;
@@ -59,54 +73,47 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const flo
             }
             float F2;
             if constexpr (!WIDE) {
-                // exact integer arithmetic in the FP32 significand; the biased
-                // float's bit pattern is the (offset) table index
-                const float fi = __fmaf_rn(A.n, sHf, __fmaf_rn(B.n, sKf, C.n + P.magic_cf));
-                F2 = __ldg(tab + __float_as_uint(fi));
+                // M + cell0 + (jA sH + jB sK + jC), exact in the FP32 significand;
+                // its bit pattern minus 0x4B400000 is the cell (tab_biased absorbs it)
+                const float fi = __fmaf_rn(A.j, sHf, __fmaf_rn(B.j, sKf, C.m));
+                F2 = __ldg(tab_biased + __float_as_uint(fi));
             } else {
-                const int idx = (__float2int_rn(A.n) - P.lo[0]) * P.sH +
-                                (__float2int_rn(B.n) - P.lo[1]) * P.sK + (__float2int_rn(C.n) - P.lo[2]);
-                F2 = __ldg(tab + idx);
+                const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
+                F2 = __ldg(base + off);
             }
-            accf = __fmaf_rn(F2 * c.z, L2, accf);
+            accf = __fmaf_rn(F2 * c.y, L2, accf);
         }
         dacc += (double)accf;
     }
     return dacc;
 }
 
-template <int SHAPE, bool WIDE>
+template <int SHAPE>
 __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
                                                  double Sa, double Sb, double Sc) {
     const double Na = P.n_cells_d[0], Nb = P.n_cells_d[1], Nc = P.n_cells_d[2];
     const double* __restrict__ tab = static_cast<const double*>(P.table);
-    const double sHd = (double)P.sH, sKd = (double)P.sK;
+    const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
     double acc = 0.0;
 #pragma unroll 2
     for (int w = 0; w < P.n_src; ++w) {
         const double2 c = sch[w];
-        const AxisF64 A = axis_f64(Sa, c.x, Na);
-        const AxisF64 B = axis_f64(Sb, c.x, Nb);
-        const AxisF64 C = axis_f64(Sc, c.x, Nc);
+        const AxisF64 A = axis_f64<kPolyF64>(Sa, c.x, Na);
+        const AxisF64 B = axis_f64<kPolyF64>(Sb, c.x, Nb);
+        const AxisF64 C = axis_f64<kPolyF64>(Sc, c.x, Nc);
         double L2;
         if constexpr (SHAPE == 0) {
             const double nn = (A.num * B.num) * C.num;
             const double dd = (A.den * B.den) * C.den;
-            const double ratio = nn * rcp_f64(dd);
+            const double ratio = nn * rcp_f64<kNewtonF64>(dd);
             L2 = ratio * ratio;
         } else {
             const double x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
             L2 = shape_latt2<SHAPE, double>(x * x + y * y + z * z, P.nnn_d);
         }
-        double F2;
-        if constexpr (!WIDE) {
-            const double di = __fma_rn(A.n, sHd, __fma_rn(B.n, sKd, C.n + P.magic_cd));
-            F2 = __ldg(tab + __double2loint(di));
-        } else {
-            const int idx = (__double2int_rn(A.n) - P.lo[0]) * P.sH +
-                            (__double2int_rn(B.n) - P.lo[1]) * P.sK + (__double2int_rn(C.n) - P.lo[2]);
-            F2 = __ldg(tab + idx);
-        }
+        // integral doubles -> int on the (otherwise idle) conversion unit, index on the ALU
+        const int idx = __double2int_rz(A.n) * P.sH + __double2int_rz(B.n) * P.sK + __double2int_rz(C.n) - l0;
+        const double F2 = __ldg(tab + idx);
         acc = __fma_rn(F2 * c.y, L2, acc);
     }
     return acc;
@@ -115,13 +122,15 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 // ---------------------------------------------------------------------------
 // The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path.
 // ---------------------------------------------------------------------------
-template <int COMPUTE, int SHAPE, bool WIDE>
-__global__ void __launch_bounds__(kBlockX* kBlockY) spots_kernel(const SpotsParams P) {
+template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
+__global__ void __launch_bounds__(kBlockX* kBlockY, 3) spots_kernel(const SpotsParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.y * kBlockX + threadIdx.x;
     if constexpr (COMPUTE == 1) {
-        float4* s = reinterpret_cast<float4*>(smem_raw);
-        const float4* g = static_cast<const float4*>(P.chan);
+        ChunkF32* k = reinterpret_cast<ChunkF32*>(smem_raw);
+        for (int i = tid; i < P.n_chunks; i += kBlockX * kBlockY) k[i] = P.chunks[i];
+        float2* s = reinterpret_cast<float2*>(smem_raw + 16 * P.n_chunks);
+        const float2* g = static_cast<const float2*>(P.chan);
         for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
     } else {
         double2* s = reinterpret_cast<double2*>(smem_raw);
@@ -180,9 +189,11 @@ __global__ void __launch_bounds__(kBlockX* kBlockY) spots_kernel(const SpotsPara
                     const double Sb = r0 * __ldg(B + 3) + r1 * __ldg(B + 4) + rr2 * __ldg(B + 5);
                     const double Sc = r0 * __ldg(B + 6) + r1 * __ldg(B + 7) + rr2 * __ldg(B + 8);
                     if constexpr (COMPUTE == 1) {
-                        sub += domain_sum_f32<SHAPE, WIDE>(P, reinterpret_cast<const float4*>(smem_raw), Sa, Sb, Sc);
+                        sub += domain_sum_f32<SHAPE, WIDE, PDEG>(
+                            P, reinterpret_cast<const ChunkF32*>(smem_raw),
+                            reinterpret_cast<const float2*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
                     } else {
-                        sub += domain_sum_f64<SHAPE, WIDE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
+                        sub += domain_sum_f64<SHAPE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
                     }
                 }
                 acc += sub * factor;
@@ -255,9 +266,9 @@ __global__ void add_array_kernel(double* __restrict__ lhs, const float* __restri
 // ---------------------------------------------------------------------------
 // Host-side launchers (C++ linkage, used by nbx_runtime.cu).
 // ---------------------------------------------------------------------------
-template <int COMPUTE, int SHAPE, bool WIDE>
+template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
 static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) {
-    auto k = spots_kernel<COMPUTE, SHAPE, WIDE>;
+    auto k = spots_kernel<COMPUTE, SHAPE, WIDE, PDEG>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -271,19 +282,23 @@ static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) 
 template <int COMPUTE, bool WIDE>
 static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cudaStream_t st) {
     switch (shape) {
-        case 0: return launch_t<COMPUTE, 0, WIDE>(P, smem, st);
-        case 1: return launch_t<COMPUTE, 1, WIDE>(P, smem, st);
-        case 2: return launch_t<COMPUTE, 2, WIDE>(P, smem, st);
-        default: return launch_t<COMPUTE, 3, WIDE>(P, smem, st);
+        case 0: return launch_t<COMPUTE, 0, WIDE, kPolyF32>(P, smem, st);
+        case 1: return launch_t<COMPUTE, 1, WIDE, kPolyF32>(P, smem, st);
+        case 2: return launch_t<COMPUTE, 2, WIDE, kPolyF32>(P, smem, st);
+        default: return launch_t<COMPUTE, 3, WIDE, kPolyF32>(P, smem, st);
     }
 }
 
+// compute: 0 FP64, 1 FP32, 2 FP32 with the degree-4 (ulp-grade) polynomial, sincg only
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st) {
-    const size_t smem = (size_t)P.n_src * 16;
-    if (compute == 1) {
-        return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);
+    if (compute == 0) {
+        const size_t smem = (size_t)P.n_src * 16;
+        return launch_shape<0, false>(P, shape, smem, st);
     }
-    return wide ? launch_shape<0, true>(P, shape, smem, st) : launch_shape<0, false>(P, shape, smem, st);
+    const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 8;
+    if (compute == 2 && shape == 0)
+        return wide ? launch_t<1, 0, true, 4>(P, smem, st) : launch_t<1, 0, false, 4>(P, smem, st);
+    return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);
 }
 
 static int grid_for(int64_t n, int block) {
@@ -319,6 +334,36 @@ __global__ void noise_kernel(const void* __restrict__ mean, void* __restrict__ o
 cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
                          cudaStream_t st) {
     noise_kernel<<<grid_for(n, 256), 256, 0, st>>>(mean, out, n, dtype, seed, image);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// FMA-throughput probe (roofline denominator).  8 independent chains per
+// thread, 16-deep unroll, 2048 threads per SM on every SM.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) fma_probe_kernel(T* out, int iters, T a, T b) {
+    T x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = (T)(threadIdx.x + c) * (T)1e-3;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = fma(x[c], a, b);
+        }
+    }
+    T s = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s += x[c];
+    if (s == (T)-1.2345) out[0] = s;  // never true; keeps the chains alive
+}
+
+cudaError_t launch_fma_probe(int fp64, void* out, int iters, int blocks, cudaStream_t st) {
+    if (fp64)
+        fma_probe_kernel<double><<<blocks, 512, 0, st>>>(static_cast<double*>(out), iters, 0.9999999, 1e-7);
+    else
+        fma_probe_kernel<float><<<blocks, 512, 0, st>>>(static_cast<float*>(out), iters, 0.9999f, 1e-4f);
     return cudaGetLastError();
 }
 

@@ -24,6 +24,14 @@ struct DevPanel {
     double inv_atten;              // 1 / attenuation_length (0 when thin)
 };
 
+// FP32 path: channels [begin, end) share the FP64 phase anchor iv0 = 1/lambda0;
+// the host sorts channels by 1/lambda and cuts chunks so that
+// |h_w - h_0| <= 1.5 for every reachable pixel and domain (|x| stays < 2).
+struct ChunkF32 {
+    double iv0;
+    int32_t begin, end;
+};
+
 // Everything the spot kernel reads.  All pointers are device pointers.
 struct SpotsParams {
     const DevPanel* panels;
@@ -32,8 +40,11 @@ struct SpotsParams {
     const double* bases;           // n_dom x 9, rows a, b, c
     int32_t n_dom;
     int32_t n_src;                 // channels in this launch (already sharded)
-    const void* chan;              // FP64: double2 {1/lambda, w}; FP32: float4 {iv_hi, iv_lo, w, 0}
-    const void* table;             // dense F^2 grid (FP32: scaled by sigma), biased base (see runtime)
+    const void* chan;              // FP64: double2 {1/lambda, w}; FP32: float2 {1/lambda - 1/lambda0, w}
+    const ChunkF32* chunks;        // FP32 only: channel chunks sharing one phase anchor 1/lambda0
+    int32_t n_chunks;
+    int32_t pad1;
+    const void* table;             // dense F^2 grid (FP32: scaled by sigma)
     double beam[3];
     int32_t pol_on;
     int32_t out_mode;              // NBX_OUT_*
@@ -44,8 +55,7 @@ struct SpotsParams {
     // dense-grid index: idx = (n_h - lo_h) * sH + (n_k - lo_k) * sK + (n_l - lo_l)
     int32_t lo[3];
     int32_t sH, sK;
-    float magic_cf;                // FP32 magic-index constant (see runtime)
-    double magic_cd;               // FP64 magic-index constant
+    float pad2;
     double out_scale;              // r_e^2 fluence / norm (/ sigma on the FP32 path)
     void* out;
     unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none

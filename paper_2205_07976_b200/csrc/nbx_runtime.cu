@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -27,6 +28,7 @@ cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode
 cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStream_t st);
 cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
                          cudaStream_t st);
+cudaError_t launch_fma_probe(int fp64, void* out, int iters, int blocks, cudaStream_t st);
 }  // namespace nbx
 
 namespace {
@@ -79,10 +81,11 @@ struct Ctx {
 struct Plan {
     Ctx* ctx = nullptr;
     int compute = 0;
+    int kernel_variant = 0;  // 0 FP64, 1 FP32, 2 FP32 with the degree-4 polynomial (NBX_FP32_POLY=4)
     int shape = 0;
     bool wide = false;
     nbx::SpotsParams P{};
-    DevBuf panels, bases, chan, table;
+    DevBuf panels, bases, chan, chunks, table;
     int64_t n_pixels = 0;
     int64_t steps = 0;
     nbx_plan_info_t info{};
@@ -202,6 +205,11 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
     try {
         plan->ctx = ctx;
         plan->compute = compute;
+        plan->kernel_variant = compute == NBX_COMPUTE_FP32 ? 1 : 0;
+        if (compute == NBX_COMPUTE_FP32) {
+            const char* ev = std::getenv("NBX_FP32_POLY");
+            if (ev && std::atoi(ev) == 4) plan->kernel_variant = 2;
+        }
         plan->shape = d->shape;
         nbx::SpotsParams& P = plan->P;
         const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
@@ -281,8 +289,12 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
         for (int a = 0; a < 3; ++a) P.lo[a] = -hmax[a];
         P.sK = (int32_t)dims[2];
         P.sH = (int32_t)(dims[1] * dims[2]);
-        const bool wide32 = cells > (int64_t(1) << 22);
+        // FP32 magic index: every cell + offset (|j| <= 2) must stay inside the 2^22 window
+        const bool wide32 = cells + 2 * ((int64_t)P.sH + P.sK + 1) >= (int64_t(1) << 22);
         plan->wide = (compute == NBX_COMPUTE_FP32) ? wide32 : false;
+        double smax = 0.0;  // largest |rel . a| over domains and axes (Angstrom)
+        for (int dd = 0; dd < d->n_domains; ++dd)
+            for (int a = 0; a < 3; ++a) smax = std::max(smax, norm3(d->bases + 9 * dd + 3 * a) * relmax);
 
         // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma)
         const double def2 = d->default_f * d->default_f;
@@ -312,17 +324,36 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
 
         // channels
         if (compute == NBX_COMPUTE_FP32) {
-            std::vector<float> ch(4 * (size_t)n_src);
+            // sort by 1/lambda and cut chunks whose phase offsets stay small:
+            // |S (iv - iv0)| <= smax (max - min) / 2 <= 1 -> |x| <= 1.5 in the kernel
+            std::vector<int> order(n_src);
+            std::vector<double> iv(n_src);
             for (int i = 0; i < n_src; ++i) {
-                const double iv = 1.0 / d->wavelengths[sb + i];  // kernels.py:257
-                const float hi = (float)iv;
-                ch[4 * i + 0] = hi;
-                ch[4 * i + 1] = (float)(iv - (double)hi);
-                ch[4 * i + 2] = (float)d->weights[sb + i];
-                ch[4 * i + 3] = 0.f;
+                order[i] = i;
+                iv[i] = 1.0 / d->wavelengths[sb + i];  // kernels.py:257
+            }
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return iv[x] < iv[y]; });
+            std::vector<nbx::ChunkF32> chunks;
+            std::vector<float> ch(2 * (size_t)n_src);
+            int i0 = 0;
+            while (i0 < n_src) {
+                int i1 = i0 + 1;
+                while (i1 < n_src && i1 - i0 < 64 && (iv[order[i1]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++i1;
+                const double iv0 = 0.5 * (iv[order[i0]] + iv[order[i1 - 1]]);
+                chunks.push_back(nbx::ChunkF32{iv0, i0, i1});
+                for (int q = i0; q < i1; ++q) {
+                    ch[2 * q + 0] = (float)(iv[order[q]] - iv0);
+                    ch[2 * q + 1] = (float)d->weights[sb + order[q]];
+                }
+                i0 = i1;
             }
             plan->chan.ensure(ch.size() * sizeof(float));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(float), cudaMemcpyHostToDevice));
+            plan->chunks.ensure(chunks.size() * sizeof(nbx::ChunkF32));
+            NBX_CUDA(cudaMemcpy(plan->chunks.p, chunks.data(), chunks.size() * sizeof(nbx::ChunkF32),
+                                cudaMemcpyHostToDevice));
+            P.chunks = static_cast<const nbx::ChunkF32*>(plan->chunks.p);
+            P.n_chunks = (int32_t)chunks.size();
             std::vector<float> tf(cells);
             for (int64_t i = 0; i < cells; ++i) tf[i] = (float)(f2[i] * sigma);
             plan->table.ensure(cells * sizeof(float));
@@ -361,17 +392,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
         P.nnn_d = (double)d->n_cells[0] * d->n_cells[1] * d->n_cells[2];
         P.nnn_f = (float)P.nnn_d;
         P.pol_on = d->polarization_on ? 1 : 0;
-        // magic-index constants: all partial sums stay in [M, M + cells)
-        const double part = -(double)P.lo[0] * P.sH - (double)P.lo[1] * P.sK - (double)P.lo[2];
-        P.magic_cf = (float)(12582912.0 + part);          // 1.5 * 2^23
-        P.magic_cd = 6755399441055744.0 + part;           // 1.5 * 2^52
-        if (compute == NBX_COMPUTE_FP32 && !plan->wide) {
-            // index = float bits - 0x4B400000: bias the base pointer instead
-            P.table = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(plan->table.p) -
-                                                    (uintptr_t)0x4B400000u * sizeof(float));
-        } else {
-            P.table = plan->table.p;
-        }
+        P.table = plan->table.p;
         P.max_slow = max_slow;
         P.max_fast = max_fast;
         P.out_scale = plan->out_scale;
@@ -422,7 +443,7 @@ int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
     P.out = dout;
     P.fault = static_cast<unsigned long long*>(ctx->fault.p);
     NBX_CUDA(cudaEventRecord(ctx->ev0, st));
-    NBX_CUDA(nbx::launch_spots(P, plan->compute, plan->shape, plan->wide, st));
+    NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
     NBX_CUDA(cudaEventRecord(ctx->ev1, st));
     plan->timed = true;
     unsigned long long fault = ~0ull;
@@ -725,6 +746,35 @@ int nbx_poisson_host(const void* mean, void* out, int64_t n, int dtype, uint64_t
             static_cast<float*>(out)[p] = (float)k;
     }
     return NBX_OK;
+}
+
+int nbx_probe_fma_peak(void* ctxp, int fp64, double* tflops) {
+    return guarded(ctxp, [&] {
+        if (!ctxp || !tflops) throw ArgError("invalid probe arguments");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        int sms = 0;
+        NBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int blocks = sms * 4;  // 4 x 512 threads = 2048 per SM
+        DevBuf sink;
+        sink.ensure(16);
+        cudaStream_t s = ctx->stream;
+        const int iters = fp64 ? 600 : 1200;
+        NBX_CUDA(nbx::launch_fma_probe(fp64, sink.p, iters / 10, blocks, s));  // warm-up
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            NBX_CUDA(cudaEventRecord(ctx->ev0, s));
+            NBX_CUDA(nbx::launch_fma_probe(fp64, sink.p, iters, blocks, s));
+            NBX_CUDA(cudaEventRecord(ctx->ev1, s));
+            NBX_CUDA(cudaEventSynchronize(ctx->ev1));
+            float ms = 0.f;
+            NBX_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            best = std::min(best, ms);
+        }
+        const double flops = 2.0 * 8 * 16 * (double)iters * blocks * 512;
+        *tflops = flops / (best * 1e-3) / 1e12;
+        return NBX_OK;
+    });
 }
 
 }  // extern "C"

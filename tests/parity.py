@@ -63,6 +63,9 @@ def metrics(got: np.ndarray, ref: np.ndarray, dims) -> dict:
     got = np.asarray(got, dtype=np.float64).reshape(-1)
     ref = np.asarray(ref, dtype=np.float64).reshape(-1)
     tot = abs(got.sum() - ref.sum()) / abs(ref.sum()) if ref.sum() != 0 else abs(got.sum())
+    if ref.max() <= 0:
+        z = float(np.abs(got).max())
+        return {"total": tot, "spot": z, "n_spots": 0, "pix_abs_over_max": z, "pix_rel_bright": z}
     labels, n = spot_labels(ref, dims)
     spot = 0.0
     if n:
