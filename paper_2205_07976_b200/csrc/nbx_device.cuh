@@ -14,7 +14,8 @@
 //     enters the image, so all signs (-1)^n, (-1)^k drop out.
 //   * The reference's limit branch (|sin x| < 1e-12 -> N cos(Nx)/cos(x)) is the
 //     t -> 0 limit of the same ratio; biasing |t| by a tiny constant makes the
-//     ratio evaluate to N there with no branch.
+//     ratio evaluate to N there.  The hot loops skip the bias (t == 0 then gives
+//     0/0) and the caller re-runs only a non-finite partial sum with it.
 //   * FP32 path: the phase is anchored per (pixel, domain, channel chunk) in
 //     FP64 (h0 = S / lambda0 = n0 + f0), and per channel only the small offset
 //     x = f0 + S (1/lambda_w - 1/lambda0) is formed in FP32 (|x| <= 2 by the
@@ -116,13 +117,15 @@ struct AxisF64 {
     double num, den, n, t;
 };
 
-template <int DEG>
+// BIAS = false in the hot loop (|t| used as is; t == 0 gives 0/0, caught by the
+// caller), true in the rare re-evaluation that reproduces the limit branch.
+template <int DEG, bool BIAS>
 __device__ __forceinline__ AxisF64 axis_f64(double S, double iv, double N) {
     AxisF64 a;
     const double h = S * iv;                      // kernels.py:257-260 (sa * (1/lambda))
     a.n = round_half_away(h);                     // lookup index, reference rounding
     a.t = h - a.n;                                // exact (Sterbenz)
-    const double ta = fabs(a.t) + kTBiasF64;
+    const double ta = BIAS ? fabs(a.t) + kTBiasF64 : fabs(a.t);
     const double k = rint(N * ta);
     const double r = __fma_rn(N, ta, -k);         // N t - k, one rounding
     a.num = r * q_sinpi_f64<DEG>(r * r);
@@ -140,14 +143,14 @@ struct AxisF32 {
 
 // `magic` is kMagicF32 or kMagicF32 + (integer < 2^22): m then carries that
 // integer offset for free (the index chain uses it to fold in the chunk's cell).
-template <int DEG>
+template <int DEG, bool BIAS>
 __device__ __forceinline__ AxisF32 axis_f32(float S_hi, float D, float f0, float N, float magic = kMagicF32) {
     AxisF32 a;
     const float x = __fmaf_rn(S_hi, D, f0);
     a.m = __fadd_rn(x, magic);
     a.j = __fsub_rn(a.m, magic);                  // rint(x), exact
     a.t = __fsub_rn(x, a.j);                      // exact
-    const float ta = fabsf(a.t) + kTBiasF32;
+    const float ta = BIAS ? fabsf(a.t) + kTBiasF32 : fabsf(a.t);
     const float k = __fsub_rn(__fmaf_rn(N, ta, kMagicF32), kMagicF32);  // rint(N t)
     const float r = __fmaf_rn(N, ta, -k);
     a.num = r * q_sinpi_f32<DEG>(r * r);

@@ -28,18 +28,60 @@ constexpr int kNewtonF64 = 1;
 
 // ---------------------------------------------------------------------------
 // Sum over channels of w * F^2 * F_latt^2 for one (pixel, sub-pixel, domain).
+//
+// The hot loops run WITHOUT the |t| bias: an exact Bragg position (t == 0 on
+// some axis, the reference's limit branch) then makes 0/0, i.e. a non-finite
+// partial sum, and only that chunk is re-evaluated with the bias, which
+// yields the analytic limit N.  Underflow of the three-axis products is
+// caught the same way.
+//
 // FP32 path: channels come in chunks with one FP64 phase anchor each; the
-// chunk's F^2 base pointer is biased so that the magic-number float built by
-// the index FMA chain is directly the byte offset / 4.
+// l-axis magic carries the chunk's cell so that the float built by the index
+// FMA chain is directly the biased cell number.
 // ---------------------------------------------------------------------------
+template <int SHAPE, bool WIDE, int PDEG, bool BIAS>
+__device__ __forceinline__ float chunk_sum_f32(const SpotsParams& P, const float2* __restrict__ sch, int w0, int w1,
+                                               float a_hi, float b_hi, float c_hi, float fa, float fb, float fc,
+                                               float magic_c, const float* __restrict__ base) {
+    const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
+    const float sHf = (float)P.sH, sKf = (float)P.sK;
+    float accf = 0.0f;
+#pragma unroll 4
+    for (int w = w0; w < w1; ++w) {
+        const float2 c = sch[w];
+        const AxisF32 A = axis_f32<PDEG, BIAS>(a_hi, c.x, fa, Na);
+        const AxisF32 B = axis_f32<PDEG, BIAS>(b_hi, c.x, fb, Nb);
+        const AxisF32 C = axis_f32<PDEG, BIAS>(c_hi, c.x, fc, Nc, magic_c);
+        float L2;
+        if constexpr (SHAPE == 0) {
+            const float nn = (A.num * B.num) * C.num;
+            const float dd = (A.den * B.den) * C.den;
+            const float ratio = nn * rcp_approx_f32(dd);
+            L2 = ratio * ratio;
+        } else {
+            const float x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
+            L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn_f);
+        }
+        float F2;
+        if constexpr (!WIDE) {
+            // M + cell0 + (jA sH + jB sK + jC), exact in the FP32 significand;
+            // its bit pattern minus 0x4B400000 is the cell (base is biased by that)
+            const float fi = __fmaf_rn(A.j, sHf, __fmaf_rn(B.j, sKf, C.m));
+            F2 = __ldg(base + __float_as_uint(fi));
+        } else {
+            const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
+            F2 = __ldg(base + off);
+        }
+        accf = __fmaf_rn(F2 * c.y, L2, accf);
+    }
+    return accf;
+}
+
 template <int SHAPE, bool WIDE, int PDEG>
 __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const ChunkF32* __restrict__ sck,
                                                  const float2* __restrict__ sch, double Sa, double Sb,
                                                  double Sc) {
     const float a_hi = __double2float_rn(Sa), b_hi = __double2float_rn(Sb), c_hi = __double2float_rn(Sc);
-    const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
-    const float sHf = (float)P.sH, sKf = (float)P.sK;
-    const float* tab_biased = static_cast<const float*>(P.table) - (int64_t)0x4B400000;
     double dacc = 0.0;
     for (int ci = 0; ci < P.n_chunks; ++ci) {
         const ChunkF32 ck = sck[ci];
@@ -50,47 +92,25 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         const float fb = __double2float_rn(hb - (double)nb);
         const float fc = __double2float_rn(hc - (double)nc);
         const int64_t cell0 = (int64_t)(na - P.lo[0]) * P.sH + (int64_t)(nb - P.lo[1]) * P.sK + (nc - P.lo[2]);
-        // !WIDE: the l-axis magic carries cell0, so float_bits(M + cell0 + offset)
-        // - 0x4B400000 is the absolute cell; WIDE: per-chunk base + int offset
+        // !WIDE: the l-axis magic carries cell0 and base absorbs the float bias;
+        // WIDE: per-chunk base + integer offset
         const float magic_c = WIDE ? kMagicF32 : kMagicF32 + (float)cell0;
-        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : 0);
-        float accf = 0.0f;
-#pragma unroll 2
-        for (int w = ck.begin; w < ck.end; ++w) {
-            const float2 c = sch[w];
-            const AxisF32 A = axis_f32<PDEG>(a_hi, c.x, fa, Na);
-            const AxisF32 B = axis_f32<PDEG>(b_hi, c.x, fb, Nb);
-            const AxisF32 C = axis_f32<PDEG>(c_hi, c.x, fc, Nc, magic_c);
-            float L2;
-            if constexpr (SHAPE == 0) {
-                const float nn = (A.num * B.num) * C.num;
-                const float dd = (A.den * B.den) * C.den;
-                const float ratio = nn * rcp_approx_f32(dd);
-                L2 = ratio * ratio;
-            } else {
-                const float x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
-                L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn_f);
-            }
-            float F2;
-            if constexpr (!WIDE) {
-                // M + cell0 + (jA sH + jB sK + jC), exact in the FP32 significand;
-                // its bit pattern minus 0x4B400000 is the cell (tab_biased absorbs it)
-                const float fi = __fmaf_rn(A.j, sHf, __fmaf_rn(B.j, sKf, C.m));
-                F2 = __ldg(tab_biased + __float_as_uint(fi));
-            } else {
-                const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
-                F2 = __ldg(base + off);
-            }
-            accf = __fmaf_rn(F2 * c.y, L2, accf);
+        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : -(int64_t)0x4B400000);
+        float accf = chunk_sum_f32<SHAPE, WIDE, PDEG, false>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb,
+                                                             fc, magic_c, base);
+        if constexpr (SHAPE == 0) {
+            if (!isfinite(accf))  // exact Bragg position / underflow: the reference's limit branch
+                accf = chunk_sum_f32<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb,
+                                                              fc, magic_c, base);
         }
         dacc += (double)accf;
     }
     return dacc;
 }
 
-template <int SHAPE>
-__device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
-                                                 double Sa, double Sb, double Sc) {
+template <int SHAPE, bool BIAS>
+__device__ __forceinline__ double channel_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
+                                                  double Sa, double Sb, double Sc) {
     const double Na = P.n_cells_d[0], Nb = P.n_cells_d[1], Nc = P.n_cells_d[2];
     const double* __restrict__ tab = static_cast<const double*>(P.table);
     const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
@@ -98,9 +118,9 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 #pragma unroll 2
     for (int w = 0; w < P.n_src; ++w) {
         const double2 c = sch[w];
-        const AxisF64 A = axis_f64<kPolyF64>(Sa, c.x, Na);
-        const AxisF64 B = axis_f64<kPolyF64>(Sb, c.x, Nb);
-        const AxisF64 C = axis_f64<kPolyF64>(Sc, c.x, Nc);
+        const AxisF64 A = axis_f64<kPolyF64, BIAS>(Sa, c.x, Na);
+        const AxisF64 B = axis_f64<kPolyF64, BIAS>(Sb, c.x, Nb);
+        const AxisF64 C = axis_f64<kPolyF64, BIAS>(Sc, c.x, Nc);
         double L2;
         if constexpr (SHAPE == 0) {
             const double nn = (A.num * B.num) * C.num;
@@ -115,6 +135,16 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
         const int idx = __double2int_rz(A.n) * P.sH + __double2int_rz(B.n) * P.sK + __double2int_rz(C.n) - l0;
         const double F2 = __ldg(tab + idx);
         acc = __fma_rn(F2 * c.y, L2, acc);
+    }
+    return acc;
+}
+
+template <int SHAPE>
+__device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
+                                                 double Sa, double Sb, double Sc) {
+    double acc = channel_sum_f64<SHAPE, false>(P, sch, Sa, Sb, Sc);
+    if constexpr (SHAPE == 0) {
+        if (!isfinite(acc)) acc = channel_sum_f64<SHAPE, true>(P, sch, Sa, Sb, Sc);
     }
     return acc;
 }

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -100,6 +101,11 @@ struct Plan {
 // (model.py:328-406, kernels.py:204-208) so the same bad inputs fail.
 // --------------------------------------------------------------------------
 bool finite(double x) { return std::isfinite(x); }
+
+bool trace_enabled() {
+    static const bool on = std::getenv("NBX_TRACE") != nullptr;
+    return on;
+}
 
 double norm3(const double* v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
 
@@ -617,14 +623,24 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
         if (!ctxp) throw ArgError("NULL context");
         NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
         check_mode(out_mode);
+        const auto t0 = std::chrono::steady_clock::now();
         Plan* plan = build_plan(static_cast<Ctx*>(ctxp), d, compute);
+        const auto t1 = std::chrono::steady_clock::now();
         try {
             bad = run_plan(plan, out_mode, out, out_on_device);
         } catch (...) {
             delete plan;
             throw;
         }
+        const auto t2 = std::chrono::steady_clock::now();
+        const float kms = plan->last_ms;
         delete plan;
+        if (trace_enabled()) {
+            const auto t3 = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "[nbx] spots: plan %.2f ms, run %.2f ms (kernel %.2f ms), release %.2f ms\n",
+                         ms(t0, t1), ms(t1, t2), kms, ms(t2, t3));
+        }
         return NBX_OK;
     });
     if (st != NBX_OK) return st;
