@@ -136,11 +136,27 @@ def _panels_of(panel) -> tuple:
     return panel.panels if isinstance(panel, (Detector, DetectorPanel)) else (panel,)
 
 
-def describe(ctx: SpotsContext, *, src_begin: int = 0, src_end: int = 0, norm: float = 0.0) -> N.Descriptor:
-    """Flatten a SpotsContext into the C descriptor (what the kernel reads)."""
+def _table_arrays(table) -> tuple[np.ndarray, np.ndarray]:
+    if hasattr(table, "arrays"):
+        return table.arrays()
+    # duck-typed reference StructureFactorTable (model.py:227-285): a dict of entries
+    n = len(table.entries)
+    hkl = np.array(list(table.entries.keys()), dtype=np.int32).reshape(n, 3)
+    amp = np.array(list(table.entries.values()), dtype=np.float64).reshape(n)
+    return hkl, amp
+
+
+def describe(ctx, *, src_begin: int = 0, src_end: int = 0, norm: float = 0.0) -> N.Descriptor:
+    """Flatten a SpotsContext into the C descriptor (what the kernel reads).
+
+    Accepts this package's SpotsContext or the reference's own (duck typing:
+    crystal/panel/spectrum/oversample/r_e_sqr with the reference's fields), so
+    ``nanobragg_spots(xtrace_ctx, xtrace_pixelbuffer)`` works unchanged.
+    """
     crystal, spectrum = ctx.crystal, ctx.spectrum
-    hkl, amp = crystal.sf_table.arrays()
-    bases = crystal.rotated_real_bases(ctx.phi)
+    hkl, amp = _table_arrays(crystal.sf_table)
+    phi = getattr(ctx, "phi", None)
+    bases = crystal.rotated_real_bases(phi) if phi is not None else crystal.rotated_real_bases()
     return N.Descriptor(
         panels=_panels_of(ctx.panel),
         oversample=ctx.oversample,
@@ -155,7 +171,7 @@ def describe(ctx: SpotsContext, *, src_begin: int = 0, src_end: int = 0, norm: f
         hkl=hkl,
         amplitudes=amp,
         default_f=crystal.sf_table.default_f,
-        shape=N.SHAPES[ctx.shape],
+        shape=N.SHAPES[getattr(ctx, "shape", "sincg")],
         norm=norm,
         src_begin=src_begin,
         src_end=src_end,
@@ -188,7 +204,8 @@ def nanobragg_spots(ctx: SpotsContext, out: PixelBuffer, executor=None) -> None:
     cx = N.context()
     mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
     bad = N.C.c_int64(-1)
-    status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), N.COMPUTE[ctx.compute], mode,
+    compute = N.COMPUTE[getattr(ctx, "compute", "fp64")]
+    status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), compute, mode,
                               out.data.ctypes.data, 0, N.C.byref(bad))
     N.check(cx, status, bad.value)
     if executor is not None and hasattr(executor, "timing_log"):
