@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--size", type=int, default=3840)
     ap.add_argument("--channels", type=int, default=100)
     ap.add_argument("--domains", type=int, default=50)
+    ap.add_argument("--mode", default="image", choices=["image", "channels", "jungfrau"],
+                    help="image: C2 image-sharded (default); channels: C5 one 1000-channel image channel-sharded; "
+                         "jungfrau: C4 256-panel FP64")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / fp64 / cpu-baseline legs")
     return ap.parse_args()
 
@@ -132,6 +135,10 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args):
+    if args.mode == "channels" and args.channels == 100:
+        args.channels = 1000
+    if args.mode == "jungfrau" and args.compute == "fp32" and "--compute" not in sys.argv:
+        args.compute = "fp64"
     world, rank, local = dist_env()
     os.environ["NBX_DEVICE"] = str(local)
     import numpy as np
@@ -152,17 +159,38 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     cx.lib.nbx_ctx_set_stream(cx.handle, N.C.c_void_p(stream.cuda_stream))
 
+    from paper_2205_07976_b200 import parallel
+
     size = args.size
     r0 = (3840 - size) // 2
     panel = synthetic.rayonix_panel() if size == 3840 else synthetic.roi(synthetic.rayonix_panel(), r0, r0, size, size)
+    mode = args.mode
+    if mode == "jungfrau":
+        panel = synthetic.jungfrau_detector()
 
     def ctx_for(i, compute):
-        return synthetic.ls49_context(synthetic.SEED + 100003 * rank + i, n_channels=args.channels,
-                                      n_domains=args.domains, panel=panel, compute=compute)
+        seed = synthetic.SEED + (0 if mode == "channels" else 100003 * rank) + i
+        if mode == "jungfrau":
+            return synthetic.jungfrau_context(seed, n_channels=args.channels, n_domains=args.domains,
+                                              compute=compute)
+        if mode == "channels":  # C5: 1000 channels, E_j = 7020 + 0.2 j eV
+            return synthetic.ls49_context(seed, n_channels=args.channels, n_domains=args.domains, e0=7020.0,
+                                          de=0.2, panel=panel, compute=compute)
+        return synthetic.ls49_context(seed, n_channels=args.channels, n_domains=args.domains, panel=panel,
+                                      compute=compute)
 
     n_img = args.warmup + args.steps
-    plans = [SpotsPlan(ctx_for(i, args.compute), device=local) for i in range(n_img)]
-    steps_per_image = plans[0].steps
+    if mode == "channels":
+        # every step renders ONE image with the whole job: this rank's channel shard
+        lo, hi = parallel.channel_shards(args.channels, world)[rank]
+        plans = []
+        for i in range(n_img):
+            c = ctx_for(i, args.compute)
+            plans.append(SpotsPlan(c, device=local, src_begin=lo, src_end=hi, norm=parallel.global_norm(c)))
+        raw = torch.zeros(plans[0].n_pixels, dtype=torch.float64, device="cuda")
+    else:
+        plans = [SpotsPlan(ctx_for(i, args.compute), device=local) for i in range(n_img)]
+    steps_per_unit = plans[0].steps  # per rank per step
     out = torch.empty(plans[0].n_pixels, dtype=torch.float32, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
@@ -170,11 +198,25 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    for i in range(args.warmup):
+    def one_step(i):
         flush.zero_()
-        plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+        if mode != "channels":
+            plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            return
+        raw.zero_()
+        plans[i].run(raw.data_ptr(), mode=N.OUT_RAW_F64, on_device=True)
+        if world > 1:
+            dist.reduce(raw, dst=0, op=dist.ReduceOp.SUM)
+        if rank == 0:
+            bad = N.C.c_int64(-1)
+            st = cx.lib.nbx_finalize(cx.handle, raw.data_ptr(), raw.numel(), plans[i].scale, N.OUT_F32,
+                                     out.data_ptr(), 1, N.C.byref(bad))
+            N.check(cx, st, bad.value)
 
-    # roofline denominator: live FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32 figure)
+    for i in range(args.warmup):
+        one_step(i)
+
+    # roofline denominator: live FMA probe on this GPU (MEASURED_PEAKS.json has no FP32/FP64 figure)
     peak = N.C.c_double(0.0)
     cx.lib.nbx_probe_fma_peak(cx.handle, 1 if args.compute == "fp64" else 0, N.C.byref(peak))
 
@@ -185,8 +227,7 @@ def run_ours(args):
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for i in range(args.warmup, n_img):
-            flush.zero_()
-            plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            one_step(i)
             kernel_ms.append(plans[i].kernel_ms)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -196,11 +237,12 @@ def run_ours(args):
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    total_images = world * args.steps
+    total_images = args.steps if mode == "channels" else world * args.steps
+    steps_per_image = steps_per_unit * (world if mode == "channels" else 1)
     value = total_images / (elapsed / 1e3)
     gsteps = total_images * steps_per_image / (elapsed / 1e3) / 1e9
     mean_kernel = statistics.fmean(kernel_ms)
-    achieved = STEP_INSTR * 2.0 * steps_per_image / (mean_kernel / 1e3) / 1e12
+    achieved = STEP_INSTR * 2.0 * steps_per_unit / (mean_kernel / 1e3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
@@ -208,18 +250,29 @@ def run_ours(args):
             traffic = json.loads(prof.read_text()).get(f"spots_{args.compute}", {}).get("dram_bytes_per_launch")
         except (ValueError, AttributeError):
             traffic = None
+    workload = {"image": WORKLOAD if size == 3840 else f"{WORKLOAD} (ROI {size}x{size})",
+                "channels": f"C5 single LS49-shape image, {size}x{size}, {args.channels} channels (7020 + 0.2 j eV), "
+                            f"{args.domains} mosaic domains, channel-sharded over {world} GPU(s) + NCCL reduce",
+                "jungfrau": f"C4 Jungfrau-16M-like: 256 panels x 254x254, oversample 2, 3 thickness layers, "
+                            f"{args.channels} channels, {args.domains} domains"}[mode]
+    parallelism = {"image": f"image-sharded x{world} (no collective)",
+                   "jungfrau": f"image-sharded x{world} (no collective)",
+                   "channels": f"channel-sharded x{world}, FP64 partials reduced to rank 0 (NCCL), finalize on rank 0"}
     result = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,
+        "scaling": "strong" if mode == "channels" else "weak",
         "vs_baseline": None, "dtype": "f32" if args.compute == "fp32" else "f64",
         "data": "synthetic (seeded LS49-shape crystal, Wilson Fhkl to 1.6 A, random orientation per image)",
-        "config": {"workload": WORKLOAD if size == 3840 else f"{WORKLOAD} (ROI {size}x{size})",
-                   "images_per_gpu_per_step": 1, "global_batch": world, "steps_per_image": steps_per_image,
-                   "compute": args.compute, "parallelism": f"image-sharded x{world} (no collective)",
+        "config": {"workload": workload, "mode": mode,
+                   "images_per_gpu_per_step": 1 if mode != "channels" else 1.0 / world,
+                   "global_batch": world if mode != "channels" else 1, "steps_per_image": steps_per_image,
+                   "compute": args.compute, "parallelism": parallelism[mode],
                    "l2": "256 MB buffer written between timed images (L2 flushed); Fhkl grid L2-resident by design"},
         "gsteps_per_s": gsteps,
         "kernel_ms_mean": mean_kernel,
-        "gpu_launches": args.steps,  # one spot kernel per image; the flush is torch's fill, not ours
+        # one spot kernel per image per rank (+ one finalize on rank 0 in channel mode); the flush is torch's
+        "gpu_launches": args.steps * (2 if (mode == "channels" and rank == 0) else 1),
         "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
                      "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
                      "traffic": traffic,
@@ -228,28 +281,43 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
 
-    if rank == 0 and not args.no_extras:
-        # e2e: drop-in API, host PixelBuffer, everything inside the timed region
-        from paper_2205_07976_b200.kernels import SpotsContext
-
+    if not args.no_extras and (rank == 0 or mode == "channels"):
+        # e2e: the public API with host buffers, descriptor upload and image download inside the timed region
         e2e_steps = max(1, min(args.steps, 3))
         ctxs = [ctx_for(1000 + i, args.compute) for i in range(e2e_steps + 1)]
         img = PixelBuffer.zeros(panel.dims, "f32")
-        nanobragg_spots(ctxs[0], img)  # warm (host tables, context)
+
+        def e2e_call(c):
+            if mode == "channels":
+                parallel.simulate_channel_sharded(c, img)
+            else:
+                nanobragg_spots(c, img)
+
+        e2e_call(ctxs[0])  # warm (host tables, context)
+        barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for c in ctxs[1:]:
-            nanobragg_spots(c, img)
+            e2e_call(c)
         ev1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = ev0.elapsed_time(ev1) / e2e_steps
+        if world > 1 and mode == "channels":
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
         info = plans[0].info
         h2d = int(info.table_cells) * (4 if args.compute == "fp32" else 8) + args.channels * 16 + \
-            args.domains * 72 + 160
-        result["e2e"] = {"value": 1e3 / e2e_ms, "unit": "images/s", "h2d_bytes_per_step": h2d,
+            args.domains * 72 + 160 * len(getattr(panel, "panels", (panel,)))
+        result["e2e"] = {"value": 1e3 / e2e_ms * (1 if mode == "channels" else world), "unit": "images/s", "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": int(plans[0].n_pixels) * 4 + 8, "ms_per_step": e2e_ms,
-                         "api": "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"}
+                         "api": ("paper_2205_07976_b200.parallel.simulate_channel_sharded(ctx, PixelBuffer)"
+                                 if mode == "channels" else
+                                 "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"),
+                         "note": "rank 0's rate x n_gpus (ranks are independent)" if mode != "channels" and world > 1
+                         else "whole job"}
 
+    if rank == 0 and not args.no_extras and mode == "image" and args.compute == "fp32":
         # FP64 path on the same workload (the 1e-9 parity path)
         p64 = SpotsPlan(ctx_for(0, "fp64"), device=local)
         p64.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
@@ -267,8 +335,8 @@ def run_ours(args):
                                             "unit": "TFLOP/s", "frac": ach64 / peak64.value if peak64.value else None}}
         p64.close()
 
-        if world == 1:
-            result["cpu_baseline"] = cpu_baseline_port(ctx_for(0, "fp64"), panel, steps_per_image, oracle)
+    if rank == 0 and not args.no_extras and world == 1:
+        result["cpu_baseline"] = cpu_baseline_port(ctx_for(0, "fp64"), panel, steps_per_image, oracle)
 
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -279,25 +347,27 @@ def run_ours(args):
 
 
 def cpu_baseline_port(ctx, panel, steps_per_image, oracle):
-    """The C oracle (FP64 scalar restatement) on all host cores over a 16-row ROI of the image."""
-    from paper_2205_07976_b200 import describe, synthetic
-
-    rows = 16
-    r0 = panel.slow_pixels // 2 - rows // 2
+    """The C oracle (FP64 scalar restatement) on all host cores over a bounded row sample of the image."""
     import dataclasses
 
-    sub = dataclasses.replace(ctx, panel=synthetic.roi(panel, r0, 0, rows, panel.fast_pixels))
+    from paper_2205_07976_b200 import describe, synthetic
+
+    per_pixel = steps_per_image // panel.n_pixels  # every pixel costs the same number of steps
+    one = panel.panels[0] if hasattr(panel, "panels") and len(panel.panels) > 1 else panel
+    rows = 16 if per_pixel <= 10000 else 4
+    r0 = one.slow_pixels // 2 - rows // 2
+    sub = dataclasses.replace(ctx, panel=synthetic.roi(one, r0, 0, rows, one.fast_pixels))
     desc = describe(sub)
     cores = host_cores()
     t0 = time.perf_counter()
     oracle.spots(desc, "f32", nthreads=cores)
     dt = time.perf_counter() - t0
-    sample_steps = rows * panel.fast_pixels * steps_per_image // panel.n_pixels
+    sample_steps = rows * one.fast_pixels * per_pixel
     sps = sample_steps / dt
     return {"value": sps / steps_per_image, "unit": "images/s", "cores": cores, "kind": "port",
             "gsteps_per_s": sps / 1e9, "seconds": dt, "cpu": cpu_model(),
-            "sample": f"rows {r0}-{r0 + rows - 1} x {panel.fast_pixels} px x all sources x all domains "
-                      f"({sample_steps:.3g} steps) of the same image, oracle/nbx_oracle.c FP64, {cores} threads"}
+            "sample": f"rows {r0}-{r0 + rows - 1} x {one.fast_pixels} px (panel 0) x every sub-pixel/layer/source/"
+                      f"domain ({sample_steps:.3g} steps) of the same image, oracle/nbx_oracle.c FP64, {cores} threads"}
 
 
 # ----------------------------------------------------------------------------- reference arm

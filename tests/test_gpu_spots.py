@@ -282,3 +282,74 @@ def test_poisson_noise_bit_exact_with_host_twin(gpu):
     flat = PixelBuffer((1, 200000), "f64", np.full(200000, 37.5))
     draws = add_noise(flat, seed=9).data
     assert abs(draws.mean() - 37.5) < 0.1 and abs(draws.var() - 37.5) < 1.0
+
+
+def test_channel_sharded_path_single_rank(gpu):
+    """The C5 path (raw FP64 partial -> reduce -> nbx_finalize) on one rank equals the direct image."""
+    from paper_2205_07976_b200 import parallel
+
+    ctx = roi_ctx()
+    direct = run(ctx, "f64").data
+    got = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(ctx.panel.dims, "f64"))
+    np.testing.assert_allclose(got.data, direct, rtol=1e-13, atol=0)
+    f32 = parallel.simulate_channel_sharded(ctx)
+    assert f32.precision == "f32"
+    np.testing.assert_allclose(f32.data, direct.astype(np.float32), rtol=2e-7)
+
+
+def test_nanobragg_facade_matches_api(gpu):
+    from paper_2205_07976_b200 import nanoBragg, shapetype
+
+    sim = nanoBragg(detpixels_slowfast=(48, 40), pixel_size_mm=0.1, Ncells_abc=(5, 6, 7), oversample=2)
+    sim.distance_mm = 90.0
+    sim.wavelength_A = 1.1
+    sim.unit_cell_tuple = (60, 70, 80, 90, 95, 90)
+    sim.mosaic_spread_deg, sim.mosaic_domains, sim.mosaic_seed = 0.1, 3, 5
+    sim.Fhkl_tuple = ([(1, 0, 0), (0, 1, 1)], [200.0, 90.0])
+    sim.default_F = 10.0
+    sim.add_nanoBragg_spots()
+    want = run(sim.to_context(), "f64").as_image()
+    assert np.array_equal(sim.raw_pixels, want)
+    sim.add_nanoBragg_spots()
+    assert np.array_equal(sim.raw_pixels, 2 * want)
+    sim.xtal_shape = shapetype.Gauss
+    assert sim.to_context().shape == "gauss"
+    sim.seed = 3
+    before = sim.raw_pixels.copy()
+    sim.add_noise()
+    assert np.all(sim.raw_pixels == np.round(sim.raw_pixels)) and not np.array_equal(before, sim.raw_pixels)
+
+
+def test_reference_duck_typed_context(gpu):
+    """The drop-in accepts reference-shaped objects (no PhiScan / arrays() / compute fields)."""
+    import types
+
+    case = parity.load("scalar_match")
+    ours = parity.context(case)
+    table = types.SimpleNamespace(entries=dict(ours.crystal.sf_table.entries),
+                                  default_f=ours.crystal.sf_table.default_f)
+    crystal = types.SimpleNamespace(cell=ours.crystal.cell, n_cells=ours.crystal.n_cells, sf_table=table,
+                                    mosaic=ours.crystal.mosaic,
+                                    rotated_real_bases=lambda: ours.crystal.rotated_real_bases())
+    ref_ctx = types.SimpleNamespace(crystal=crystal, panel=ours.panel, spectrum=ours.spectrum,
+                                    oversample=ours.oversample, r_e_sqr=ours.r_e_sqr)
+    out = types.SimpleNamespace(data=np.zeros(16, np.float32), dims=(4, 4), precision="f32")
+    nanobragg_spots(ref_ctx, out)
+    assert np.array_equal(out.data, run(ours).data)
+
+
+def test_batch_api_equals_single_images(gpu):
+    import ctypes as C
+
+    from paper_2205_07976_b200 import _native as N
+
+    ctxs = [roi_ctx(seed=synthetic.SEED + i) for i in range(3)]
+    descs = [describe(c) for c in ctxs]
+    arr = (N.SpotsDesc * 3)(*[d.c for d in descs])
+    outs = [np.zeros(c.panel.n_pixels, np.float32) for c in ctxs]
+    ptrs = (C.c_void_p * 3)(*[o.ctypes.data for o in outs])
+    cx = N.context()
+    bad = C.c_int64(-1)
+    assert cx.lib.nbx_spots_batch(cx.handle, arr, 3, 0, N.OUT_F32, ptrs, 0, C.byref(bad)) == 0
+    for c, o in zip(ctxs, outs):
+        assert np.array_equal(o, run(c).data)
