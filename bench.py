@@ -297,8 +297,11 @@ def run_ours(args):
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
+        call_ms = []
         for c in ctxs[1:]:
+            t_call = time.perf_counter()
             e2e_call(c)
+            call_ms.append(round((time.perf_counter() - t_call) * 1e3, 2))
         ev1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = ev0.elapsed_time(ev1) / e2e_steps
@@ -315,7 +318,7 @@ def run_ours(args):
                                  if mode == "channels" else
                                  "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"),
                          "note": "rank 0's rate x n_gpus (ranks are independent)" if mode != "channels" and world > 1
-                         else "whole job"}
+                         else "whole job", "call_wall_ms": call_ms}
 
     if rank == 0 and not args.no_extras and mode == "image" and args.compute == "fp32":
         # FP64 path on the same workload (the 1e-9 parity path)
