@@ -52,7 +52,10 @@ enum {
     NBX_OUT_F64 = 1,     /* out[p] = scale*acc in f64 (extension; the reference rejects f64) */
     NBX_OUT_ADD_F64 = 2, /* out[p] += f64(f32(scale*acc)): spots fused with add_array
                             (kernels.py:315-331, scheduler.py:169-174) */
-    NBX_OUT_RAW_F64 = 3  /* out[p] += acc (unscaled FP64 partial, for channel shards) */
+    NBX_OUT_RAW_F64 = 3, /* out[p] += acc (unscaled FP64 partial, for channel shards) */
+    NBX_OUT_IMAGE_F64 = 4 /* out[p] = f64(f32(spots)) + f64(f32(background)): the simulate_image
+                             accumulator (scheduler.py:156-183) in one launch; background only when
+                             the descriptor carries a profile (bg_points > 0) */
 };
 
 /* Lattice shape transforms.  SINCG is the reference's grating
@@ -112,6 +115,14 @@ typedef struct nbx_spots_desc {
     /* channel shard: evaluate sources [src_begin, src_end); src_end <= 0 -> all */
     int32_t src_begin;
     int32_t src_end;
+    /* diffuse background (add_background, kernels.py:279-312): BackgroundProfile points
+     * (stol strictly increasing, 1/Angstrom; amplitudes), used by nbx_background and by
+     * NBX_OUT_IMAGE_F64.  bg_points = 0: no background. */
+    int32_t bg_points;
+    int32_t reserved1;
+    const double* bg_stol;
+    const double* bg_f;
+    double bg_thickness_factor;
 } nbx_spots_desc;
 
 /* Filled by nbx_plan_info. */
@@ -145,6 +156,10 @@ int64_t nbx_output_pixels(const nbx_spots_desc* d);
  * the reference (execution.py:217-224). */
 int nbx_spots(void* ctx, const nbx_spots_desc* d, int compute, int out_mode,
               void* out, int out_on_device, int64_t* first_bad);
+/* With NBX_OUT_IMAGE_F64 a fault can come from either stage: *first_bad is the
+ * spot stage's lowest bad pixel if any, else the background's, and
+ * nbx_fault_stage(ctx) says which (0 spots, 1 background). */
+int nbx_fault_stage(void* ctx);
 
 /* Batch of independent images (SURVEY §8 E1 image sharding, config C3):
  * outs[i] receives image i; images share nothing and launch back to back
@@ -160,6 +175,14 @@ int nbx_plan_info(void* plan, nbx_plan_info_t* info);
 /* Device-time of the last nbx_plan_run spot kernel (ms, CUDA events). */
 double nbx_plan_last_kernel_ms(void* plan);
 void nbx_plan_destroy(void* plan);
+
+/* Diffuse background image alone -- add_background(profile, panel, spectrum,
+ * thickness_factor, out) (kernels.py:279-312): pixel centres, one interpolated
+ * f_bg(sin(theta)/lambda)^2 per source.  out_mode NBX_OUT_F32 (the reference's
+ * store) / NBX_OUT_F64 / NBX_OUT_ADD_F64 (+= f64(f32), add_array fused).
+ * Only panels, beam, spectrum, fluence, r_e_sqr and the bg_* fields are read. */
+int nbx_background(void* ctx, const nbx_spots_desc* d, int out_mode, void* out, int out_on_device,
+                   int64_t* first_bad);
 
 /* Scale + store a reduced raw FP64 image (root of a channel-sharded image,
  * SURVEY §8 E1): out = mode(scale * raw).  raw is a device pointer. */

@@ -43,6 +43,8 @@ def load():
         lib.oracle_spots.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int64)]
         lib.oracle_scale.restype = C.c_double
         lib.oracle_scale.argtypes = [C.c_void_p]
+        lib.oracle_background.restype = C.c_int
+        lib.oracle_background.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_int64)]
         lib.oracle_poisson.restype = C.c_int
         lib.oracle_poisson.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_uint64]
         _lib = lib
@@ -73,6 +75,18 @@ def spots(desc, mode: str = "f64", nthreads: int | None = None, out: np.ndarray 
     rc = lib.oracle_spots(C.addressof(c), code, out.ctypes.data, nthreads or threads(), C.byref(bad))
     if rc != 0:
         raise ValueError("oracle rejected the descriptor")
+    return out, bad.value
+
+
+def background(desc, mode: str = "f64"):
+    """add_background restated (kernels.py:279-312); desc must carry the bg_* fields."""
+    lib = load()
+    c = getattr(desc, "c", desc)
+    n = sum(c.panels[i].slow_pixels * c.panels[i].fast_pixels for i in range(c.n_panels))
+    out = np.zeros(n, dtype=np.float32 if mode == "f32" else np.float64)
+    bad = C.c_int64(-1)
+    if lib.oracle_background(C.addressof(c), 0 if mode == "f32" else 1, out.ctypes.data, C.byref(bad)) != 0:
+        raise ValueError("oracle rejected the background descriptor")
     return out, bad.value
 
 

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libnbx.so"
 
 NBX_OK, NBX_ERR_ARG, NBX_ERR_NUMERICAL, NBX_ERR_CUDA = 0, 1, 2, 3
 COMPUTE = {"fp64": 0, "fp32": 1}
-OUT_F32, OUT_F64, OUT_ADD_F64, OUT_RAW_F64 = 0, 1, 2, 3
+OUT_F32, OUT_F64, OUT_ADD_F64, OUT_RAW_F64, OUT_IMAGE_F64 = 0, 1, 2, 3, 4
 SHAPES = {"sincg": 0, "square": 0, "gauss": 1, "round": 2, "tophat": 3}
 
 # Every exported symbol of include/nbx.h (checked by tests/test_abi.py).
@@ -27,7 +27,8 @@ EXPORTS = (
     "nbx_version", "nbx_ctx_create", "nbx_ctx_destroy", "nbx_last_error", "nbx_ctx_set_stream",
     "nbx_ctx_synchronize", "nbx_output_pixels", "nbx_spots", "nbx_spots_batch", "nbx_plan_create",
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
-    "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak",
+    "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak", "nbx_background",
+    "nbx_fault_stage",
 )
 
 
@@ -50,6 +51,8 @@ class SpotsDesc(C.Structure):
         ("n_cells", C.c_int32 * 3), ("n_entries", C.c_int32), ("hkl", C.POINTER(C.c_int32)),
         ("amplitudes", C.POINTER(C.c_double)), ("default_f", C.c_double), ("norm", C.c_double),
         ("src_begin", C.c_int32), ("src_end", C.c_int32),
+        ("bg_points", C.c_int32), ("reserved1", C.c_int32), ("bg_stol", C.POINTER(C.c_double)),
+        ("bg_f", C.POINTER(C.c_double)), ("bg_thickness_factor", C.c_double),
     ]
 
 
@@ -98,6 +101,8 @@ def load() -> C.CDLL:
             "nbx_add_noise": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, C.c_uint64, C.c_uint64, C.c_int]),
             "nbx_poisson_host": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_uint64, C.c_uint64]),
             "nbx_probe_fma_peak": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
+            "nbx_background": (C.c_int, [vp, C.POINTER(SpotsDesc), C.c_int, vp, C.c_int, i64p]),
+            "nbx_fault_stage": (C.c_int, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -161,7 +166,7 @@ class Descriptor:
 
     def __init__(self, *, panels, oversample, beam_direction, polarization_on, wavelengths, weights,
                  fluence, r_e_sqr, bases, n_cells, hkl, amplitudes, default_f, shape=0, norm=0.0,
-                 src_begin=0, src_end=0):
+                 src_begin=0, src_end=0, background=None, thickness_factor=1.0):
         self._panels = (Panel * len(panels))()
         for dst, p in zip(self._panels, panels):
             dst.slow_pixels = int(p.slow_pixels)
@@ -201,6 +206,13 @@ class Descriptor:
         d.norm = float(norm)
         d.src_begin = int(src_begin)
         d.src_end = int(src_end)
+        if background is not None:  # BackgroundProfile (model.py:409-435)
+            self._bg_stol = np.ascontiguousarray(background.stol, dtype=np.float64)
+            self._bg_f = np.ascontiguousarray(background.f_bg, dtype=np.float64)
+            d.bg_points = self._bg_stol.size
+            d.bg_stol = ptr(self._bg_stol, C.c_double)
+            d.bg_f = ptr(self._bg_f, C.c_double)
+            d.bg_thickness_factor = float(thickness_factor)
         self.c = d
 
     @property
@@ -216,6 +228,8 @@ def check(ctx: Context, status: int, first_bad: int = -1, label: str = "nanobrag
         return
     msg = ctx.error()
     if status == NBX_ERR_NUMERICAL:
+        if label == "simulate_image":  # which stage of the fused image faulted
+            label = "nanobragg_spots" if ctx.lib.nbx_fault_stage(ctx.handle) == 0 else "add_background"
         cause = NumericalFault(first_bad)
         raise PatternFault(label, first_bad, cause) from cause
     if status == NBX_ERR_ARG:

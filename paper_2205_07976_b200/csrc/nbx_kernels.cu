@@ -18,7 +18,51 @@
 
 namespace nbx {
 
-enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3 };
+enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 4 };
+
+// ---------------------------------------------------------------------------
+// Diffuse background of one pixel (kernels.py:279-312): pixel-centre geometry
+// (_panel_geometry with oversample 1, :158-194), stol = sin(theta)/lambda per
+// source, np.interp of the profile (clamped ends), weighted mean of f_bg^2,
+// times r_e^2 fluence thickness_factor / sum(w) and Omega*pol.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double interp_profile(const double* __restrict__ xp, const double* __restrict__ fp, int n,
+                                                 double x) {
+    if (x <= __ldg(xp)) return __ldg(fp);
+    if (x >= __ldg(xp + n - 1)) return __ldg(fp + n - 1);
+    int lo = 0, hi = n - 1;  // xp[lo] <= x < xp[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(xp + mid) <= x) lo = mid; else hi = mid;
+    }
+    const double x0 = __ldg(xp + lo), y0 = __ldg(fp + lo);
+    const double slope = (__ldg(fp + lo + 1) - y0) / (__ldg(xp + lo + 1) - x0);
+    return slope * (x - x0) + y0;
+}
+
+__device__ __forceinline__ double background_value(const SpotsParams& P, const DevPanel& pan, int sl, int f) {
+    const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
+    const double ps = pan.pixel_size;
+    const double s_coord = (((double)sl + 0.5) - pan.bc_slow) * ps;
+    const double f_coord = (((double)f + 0.5) - pan.bc_fast) * ps;
+    const double q0 = pan.distance * b0 + s_coord * pan.slow_axis[0] + f_coord * pan.fast_axis[0];
+    const double q1 = pan.distance * b1 + s_coord * pan.slow_axis[1] + f_coord * pan.fast_axis[1];
+    const double q2 = pan.distance * b2 + s_coord * pan.slow_axis[2] + f_coord * pan.fast_axis[2];
+    const double r2 = q0 * q0 + q1 * q1 + q2 * q2;
+    const double r = sqrt(r2);
+    const double s0 = q0 / r, s1 = q1 / r, s2 = q2 / r;
+    double op = (ps * ps / r2) * fabs(s0 * pan.normal[0] + s1 * pan.normal[1] + s2 * pan.normal[2]);
+    const double c2t = fmin(fmax(s0 * b0 + s1 * b1 + s2 * b2, -1.0), 1.0);
+    if (P.pol_on) op *= 0.5 * (1.0 + c2t * c2t);
+    const double sin_theta = sqrt(0.5 * (1.0 - c2t));
+    double acc = 0.0;
+    for (int w = 0; w < P.n_bg_chan; ++w) {
+        const double2 lw = __ldg(P.bg_chan + w);  // {lambda, weight}
+        const double fbg = interp_profile(P.bg_stol, P.bg_f, P.bg_points, sin_theta / lw.x);
+        acc += lw.y * (fbg * fbg);
+    }
+    return P.bg_scale * acc * op;
+}
 
 constexpr int kBlockX = 32;
 constexpr int kBlockY = 8;
@@ -254,12 +298,47 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, 3) spots_kernel(const SpotsP
             bad = !isfinite(v);
             break;
         }
-        default: {  // raw partial for channel shards
+        case kOutRawF64: {  // raw partial for channel shards
             static_cast<double*>(P.out)[p] += acc;
+            break;
+        }
+        default: {  // kOutImageF64: simulate_image's accumulator, spots (+ background) fused
+            const float v = (float)(P.out_scale * acc);
+            bad = !isfinite(v);
+            double img = (double)v;
+            if (P.bg_points > 0) {
+                const float b = (float)background_value(P, pan, sl, f);
+                if (!isfinite(b)) atomicMin(P.fault_bg, (unsigned long long)p);
+                img += (double)b;
+            }
+            static_cast<double*>(P.out)[p] = img;
             break;
         }
     }
     if (bad) atomicMin(P.fault, (unsigned long long)p);
+}
+
+// Background alone (add_background, kernels.py:279-312).
+__global__ void __launch_bounds__(kBlockX* kBlockY) background_kernel(const SpotsParams P) {
+    const DevPanel& pan = P.panels[blockIdx.z];
+    const int f = blockIdx.x * kBlockX + threadIdx.x;
+    const int sl = blockIdx.y * kBlockY + threadIdx.y;
+    if (sl >= pan.slow || f >= pan.fast) return;
+    const int64_t p = pan.out_offset + (int64_t)sl * pan.fast + f;
+    const double v = background_value(P, pan, sl, f);
+    bool bad;
+    if (P.out_mode == kOutF64) {
+        static_cast<double*>(P.out)[p] = v;
+        bad = !isfinite(v);
+    } else {
+        const float v32 = (float)v;
+        bad = !isfinite(v32);
+        if (P.out_mode == kOutF32)
+            static_cast<float*>(P.out)[p] = v32;
+        else
+            static_cast<double*>(P.out)[p] += (double)v32;
+    }
+    if (bad) atomicMin(P.fault_bg, (unsigned long long)p);
 }
 
 // ---------------------------------------------------------------------------
@@ -336,6 +415,13 @@ static int grid_for(int64_t n, int block) {
     if (g > 148 * 32) g = 148 * 32;
     if (g < 1) g = 1;
     return (int)g;
+}
+
+cudaError_t launch_background(const SpotsParams& P, cudaStream_t st) {
+    dim3 block(kBlockX, kBlockY, 1);
+    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow + kBlockY - 1) / kBlockY, P.n_panels);
+    background_kernel<<<grid, block, 0, st>>>(P);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,

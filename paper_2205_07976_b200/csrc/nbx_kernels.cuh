@@ -60,6 +60,14 @@ struct SpotsParams {
     void* out;
     unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none
     int32_t max_slow, max_fast;
+    // diffuse background (kernels.py:279-312)
+    const double2* bg_chan;        // {lambda, w} of every source
+    const double* bg_stol;
+    const double* bg_f;
+    int32_t n_bg_chan;
+    int32_t bg_points;             // 0: no background
+    double bg_scale;               // r_e^2 fluence thickness_factor / sum(w)
+    unsigned long long* fault_bg;  // background stage's lowest non-finite pixel
 };
 
 }  // namespace nbx

@@ -30,6 +30,7 @@ cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStrea
 cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint64_t seed, uint64_t image,
                          cudaStream_t st);
 cudaError_t launch_fma_probe(int fp64, void* out, int iters, int blocks, cudaStream_t st);
+cudaError_t launch_background(const SpotsParams& P, cudaStream_t st);
 }  // namespace nbx
 
 namespace {
@@ -69,14 +70,23 @@ struct DevBuf {
     }
 };
 
+struct Plan;
+
 struct Ctx {
     int device = 0;
+    int fault_stage = 0;      // stage of the last reported fault: 0 spots, 1 background
+    Plan* oneshot = nullptr;  // device buffers reused by nbx_spots (cudaFree can stall for ~100 ms)
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DevBuf out_scratch;     // device image when the caller passes host memory
     DevBuf fault;           // one u64
     std::string err;
+};
+
+// Device copies of the background profile and the {lambda, w} table it needs.
+struct BgBufs {
+    DevBuf chan, stol, f;
 };
 
 struct Plan {
@@ -87,6 +97,7 @@ struct Plan {
     bool wide = false;
     nbx::SpotsParams P{};
     DevBuf panels, bases, chan, chunks, table;
+    BgBufs bg;
     int64_t n_pixels = 0;
     int64_t steps = 0;
     nbx_plan_info_t info{};
@@ -204,10 +215,96 @@ double max_rel(const nbx_spots_desc* d) {
     return std::sqrt(std::max(0.0, 2.0 - 2.0 * min_cos)) * (1.0 + 1e-9) + 1e-12;
 }
 
-Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
+// Per-panel kernel constants (DetectorPanel, model.py:328-371, + the X1 layers).
+std::vector<nbx::DevPanel> make_panels(const nbx_spots_desc* d, int* max_slow, int* max_fast, int64_t* n_pix,
+                                       int64_t* sub_steps) {
+    std::vector<nbx::DevPanel> hp(d->n_panels);
+    int64_t off = 0, subs = 0;
+    const int os = d->oversample < 1 ? 1 : d->oversample;
+    for (int i = 0; i < d->n_panels; ++i) {
+        const nbx_panel& s = d->panels[i];
+        nbx::DevPanel& t = hp[i];
+        std::memset(&t, 0, sizeof(t));
+        t.slow = s.slow_pixels;
+        t.fast = s.fast_pixels;
+        t.out_offset = off;
+        t.pixel_size = s.pixel_size;
+        t.distance = s.distance;
+        t.bc_slow = s.beam_center[0];
+        t.bc_fast = s.beam_center[1];
+        for (int a = 0; a < 3; ++a) {
+            t.fast_axis[a] = s.fast_axis[a];
+            t.slow_axis[a] = s.slow_axis[a];
+        }
+        t.normal[0] = s.fast_axis[1] * s.slow_axis[2] - s.fast_axis[2] * s.slow_axis[1];
+        t.normal[1] = s.fast_axis[2] * s.slow_axis[0] - s.fast_axis[0] * s.slow_axis[2];
+        t.normal[2] = s.fast_axis[0] * s.slow_axis[1] - s.fast_axis[1] * s.slow_axis[0];
+        const double* b = d->beam_direction;
+        const double sgn = (t.normal[0] * b[0] + t.normal[1] * b[1] + t.normal[2] * b[2]) < 0 ? -1.0 : 1.0;
+        for (int a = 0; a < 3; ++a) t.odet[a] = sgn * t.normal[a];
+        if (s.thickness > 0) {
+            t.thick_steps = s.thick_steps;
+            t.thick_step = s.thickness / (double)s.thick_steps;
+            t.inv_atten = 1.0 / s.attenuation_length;
+        } else {
+            t.thick_steps = 1;  // a thin sensor has exactly one layer (reference)
+            t.thick_step = 0.0;
+            t.inv_atten = 0.0;
+        }
+        const int64_t npx = (int64_t)s.slow_pixels * s.fast_pixels;
+        off += npx;
+        subs += npx * (int64_t)(os * os) * t.thick_steps;
+        *max_slow = std::max(*max_slow, s.slow_pixels);
+        *max_fast = std::max(*max_fast, s.fast_pixels);
+    }
+    *n_pix = off;
+    *sub_steps = subs;
+    return hp;
+}
+
+// Background profile checks (BackgroundProfile, model.py:409-435) + device upload.
+void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
+    P.bg_points = 0;
+    if (d->bg_points <= 0) return;
+    if (d->bg_points < 2 || !d->bg_stol || !d->bg_f) throw ArgError("background profile needs at least 2 points");
+    for (int i = 0; i < d->bg_points; ++i) {
+        if (!finite(d->bg_stol[i]) || d->bg_stol[i] < 0) throw ArgError("stol values must be >= 0");
+        if (i > 0 && !(d->bg_stol[i] > d->bg_stol[i - 1])) throw ArgError("stol values must be strictly increasing");
+        if (!finite(d->bg_f[i]) || d->bg_f[i] < 0) throw ArgError("background amplitudes must be finite and >= 0");
+    }
+    if (!finite(d->bg_thickness_factor)) throw ArgError("thickness_factor must be finite");
+    double wsum = 0.0;
+    std::vector<double> lw(2 * (size_t)d->n_sources);
+    for (int i = 0; i < d->n_sources; ++i) {
+        lw[2 * i] = d->wavelengths[i];
+        lw[2 * i + 1] = d->weights[i];
+        wsum += d->weights[i];
+    }
+    B.chan.ensure(lw.size() * sizeof(double));
+    NBX_CUDA(cudaMemcpy(B.chan.p, lw.data(), lw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    B.stol.ensure(sizeof(double) * d->bg_points);
+    B.f.ensure(sizeof(double) * d->bg_points);
+    NBX_CUDA(cudaMemcpy(B.stol.p, d->bg_stol, sizeof(double) * d->bg_points, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(B.f.p, d->bg_f, sizeof(double) * d->bg_points, cudaMemcpyHostToDevice));
+    P.bg_chan = static_cast<const double2*>(B.chan.p);
+    P.bg_stol = static_cast<const double*>(B.stol.p);
+    P.bg_f = static_cast<const double*>(B.f.p);
+    P.n_bg_chan = d->n_sources;
+    P.bg_points = d->bg_points;
+    P.bg_scale = d->r_e_sqr * d->fluence * d->bg_thickness_factor / wsum;  // kernels.py:299
+}
+
+// Build (or, with `reuse`, rebuild in place -- its device buffers only grow) a plan.
+Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = nullptr) {
     validate(d);
     if (compute != NBX_COMPUTE_FP64 && compute != NBX_COMPUTE_FP32) throw ArgError("unknown compute path");
-    auto plan = new Plan();
+    auto plan = reuse ? reuse : new Plan();
+    if (reuse) {
+        plan->P = nbx::SpotsParams{};
+        plan->info = nbx_plan_info_t{};
+        plan->wide = false;
+        plan->last_ms = -1.f;
+    }
     try {
         plan->ctx = ctx;
         plan->compute = compute;
@@ -232,46 +329,9 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
         plan->scale = d->r_e_sqr * d->fluence / norm;
 
         // panels
-        std::vector<nbx::DevPanel> hp(d->n_panels);
-        int64_t off = 0;
         int max_slow = 0, max_fast = 0;
-        int64_t sub_steps = 0;
-        for (int i = 0; i < d->n_panels; ++i) {
-            const nbx_panel& s = d->panels[i];
-            nbx::DevPanel& t = hp[i];
-            std::memset(&t, 0, sizeof(t));
-            t.slow = s.slow_pixels;
-            t.fast = s.fast_pixels;
-            t.out_offset = off;
-            t.pixel_size = s.pixel_size;
-            t.distance = s.distance;
-            t.bc_slow = s.beam_center[0];
-            t.bc_fast = s.beam_center[1];
-            for (int a = 0; a < 3; ++a) {
-                t.fast_axis[a] = s.fast_axis[a];
-                t.slow_axis[a] = s.slow_axis[a];
-            }
-            t.normal[0] = s.fast_axis[1] * s.slow_axis[2] - s.fast_axis[2] * s.slow_axis[1];
-            t.normal[1] = s.fast_axis[2] * s.slow_axis[0] - s.fast_axis[0] * s.slow_axis[2];
-            t.normal[2] = s.fast_axis[0] * s.slow_axis[1] - s.fast_axis[1] * s.slow_axis[0];
-            const double* b = d->beam_direction;
-            const double sgn = (t.normal[0] * b[0] + t.normal[1] * b[1] + t.normal[2] * b[2]) < 0 ? -1.0 : 1.0;
-            for (int a = 0; a < 3; ++a) t.odet[a] = sgn * t.normal[a];
-            if (s.thickness > 0) {
-                t.thick_steps = s.thick_steps;
-                t.thick_step = s.thickness / (double)s.thick_steps;
-                t.inv_atten = 1.0 / s.attenuation_length;
-            } else {
-                t.thick_steps = 1;  // a thin sensor has exactly one layer (reference)
-                t.thick_step = 0.0;
-                t.inv_atten = 0.0;
-            }
-            const int64_t npx = (int64_t)s.slow_pixels * s.fast_pixels;
-            off += npx;
-            sub_steps += npx * (int64_t)(os * os) * t.thick_steps;
-            max_slow = std::max(max_slow, s.slow_pixels);
-            max_fast = std::max(max_fast, s.fast_pixels);
-        }
+        int64_t off = 0, sub_steps = 0;
+        const std::vector<nbx::DevPanel> hp = make_panels(d, &max_slow, &max_fast, &off, &sub_steps);
         plan->n_pixels = off;
         plan->steps = sub_steps * (int64_t)n_src * d->n_domains;
 
@@ -402,6 +462,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
         P.max_slow = max_slow;
         P.max_fast = max_fast;
         P.out_scale = plan->out_scale;
+        setup_background(d, P, plan->bg);
 
         nbx_plan_info_t& I = plan->info;
         I.n_pixels = plan->n_pixels;
@@ -416,15 +477,15 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute) {
         I.scale = plan->scale;
         return plan;
     } catch (...) {
-        delete plan;
+        if (!reuse) delete plan;
         throw;
     }
 }
 
-size_t out_elem_bytes(int mode) { return mode == NBX_OUT_F32 ? 4 : 8; }
+size_t out_elem_bytes(int mode) { return mode == NBX_OUT_F32 ? 4 : 8; }  // F64 / ADD / RAW / IMAGE: f64
 
 void check_mode(int mode) {
-    if (mode < NBX_OUT_F32 || mode > NBX_OUT_RAW_F64) throw ArgError("unknown output mode");
+    if (mode < NBX_OUT_F32 || mode > NBX_OUT_IMAGE_F64) throw ArgError("unknown output mode");
 }
 
 // Run a plan into `out`; returns the lowest non-finite pixel or -1.
@@ -442,22 +503,25 @@ int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
         if (mode == NBX_OUT_ADD_F64 || mode == NBX_OUT_RAW_F64)
             NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, st));
     }
-    ctx->fault.ensure(sizeof(unsigned long long));
-    NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, sizeof(unsigned long long), st));
+    ctx->fault.ensure(2 * sizeof(unsigned long long));
+    NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 2 * sizeof(unsigned long long), st));
     nbx::SpotsParams P = plan->P;
     P.out_mode = mode;
     P.out = dout;
     P.fault = static_cast<unsigned long long*>(ctx->fault.p);
+    P.fault_bg = P.fault + 1;
     NBX_CUDA(cudaEventRecord(ctx->ev0, st));
     NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
     NBX_CUDA(cudaEventRecord(ctx->ev1, st));
     plan->timed = true;
-    unsigned long long fault = ~0ull;
-    NBX_CUDA(cudaMemcpyAsync(&fault, ctx->fault.p, sizeof(fault), cudaMemcpyDeviceToHost, st));
+    unsigned long long fault[2] = {~0ull, ~0ull};
+    NBX_CUDA(cudaMemcpyAsync(fault, ctx->fault.p, sizeof(fault), cudaMemcpyDeviceToHost, st));
     if (!on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
     NBX_CUDA(cudaEventElapsedTime(&plan->last_ms, ctx->ev0, ctx->ev1));
-    return fault == ~0ull ? -1 : (int64_t)fault;
+    ctx->fault_stage = fault[0] != ~0ull ? 0 : 1;
+    if (fault[0] != ~0ull) return (int64_t)fault[0];
+    return fault[1] == ~0ull ? -1 : (int64_t)fault[1];
 }
 
 thread_local std::string g_noctx_err;
@@ -536,6 +600,8 @@ void nbx_ctx_destroy(void* ctxp) {
     Ctx* ctx = static_cast<Ctx*>(ctxp);
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    delete ctx->oneshot;
+    ctx->oneshot = nullptr;
     ctx->out_scratch.release();
     ctx->fault.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -623,24 +689,85 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
         if (!ctxp) throw ArgError("NULL context");
         NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
         check_mode(out_mode);
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
         const auto t0 = std::chrono::steady_clock::now();
-        Plan* plan = build_plan(static_cast<Ctx*>(ctxp), d, compute);
+        if (!ctx->oneshot) ctx->oneshot = new Plan();
+        Plan* plan = build_plan(ctx, d, compute, ctx->oneshot);
         const auto t1 = std::chrono::steady_clock::now();
-        try {
-            bad = run_plan(plan, out_mode, out, out_on_device);
-        } catch (...) {
-            delete plan;
-            throw;
-        }
+        bad = run_plan(plan, out_mode, out, out_on_device);
         const auto t2 = std::chrono::steady_clock::now();
         const float kms = plan->last_ms;
-        delete plan;
         if (trace_enabled()) {
             const auto t3 = std::chrono::steady_clock::now();
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "[nbx] spots: plan %.2f ms, run %.2f ms (kernel %.2f ms), release %.2f ms\n",
                          ms(t0, t1), ms(t1, t2), kms, ms(t2, t3));
         }
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    return fault_status(ctxp, bad, first_bad);
+}
+
+int nbx_fault_stage(void* ctxp) { return ctxp ? static_cast<Ctx*>(ctxp)->fault_stage : 0; }
+
+int nbx_background(void* ctxp, const nbx_spots_desc* d, int out_mode, void* out, int out_on_device,
+                   int64_t* first_bad) {
+    int64_t bad = -1;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        if (out_mode != NBX_OUT_F32 && out_mode != NBX_OUT_F64 && out_mode != NBX_OUT_ADD_F64)
+            throw ArgError("background output mode must be F32, F64 or ADD_F64");
+        if (!out) throw ArgError("output buffer is NULL");
+        count_pixels(d);
+        for (int i = 0; i < d->n_panels; ++i) {
+            const nbx_panel& p = d->panels[i];
+            if (!(p.pixel_size > 0) || !(p.distance > 0)) throw ArgError("invalid panel");
+            check_unit(p.fast_axis, "fast_axis");
+            check_unit(p.slow_axis, "slow_axis");
+        }
+        check_unit(d->beam_direction, "beam_direction");
+        if (d->n_sources < 1 || !d->wavelengths || !d->weights) throw ArgError("spectrum needs samples");
+        if (d->bg_points < 2) throw ArgError("background profile needs at least 2 points");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        if (!ctx->oneshot) ctx->oneshot = new Plan();
+        Plan* plan = ctx->oneshot;
+        plan->P = nbx::SpotsParams{};
+        nbx::SpotsParams& P = plan->P;
+        int max_slow = 0, max_fast = 0;
+        int64_t npix = 0, subs = 0;
+        const std::vector<nbx::DevPanel> hp = make_panels(d, &max_slow, &max_fast, &npix, &subs);
+        plan->panels.ensure(sizeof(nbx::DevPanel) * hp.size());
+        NBX_CUDA(cudaMemcpy(plan->panels.p, hp.data(), sizeof(nbx::DevPanel) * hp.size(), cudaMemcpyHostToDevice));
+        P.panels = static_cast<const nbx::DevPanel*>(plan->panels.p);
+        P.n_panels = d->n_panels;
+        P.max_slow = max_slow;
+        P.max_fast = max_fast;
+        for (int a = 0; a < 3; ++a) P.beam[a] = d->beam_direction[a];
+        P.pol_on = d->polarization_on ? 1 : 0;
+        setup_background(d, P, plan->bg);
+        const size_t bytes = (size_t)npix * (out_mode == NBX_OUT_F32 ? 4 : 8);
+        void* dout = out;
+        if (!out_on_device) {
+            ctx->out_scratch.ensure(bytes);
+            dout = ctx->out_scratch.p;
+            if (out_mode == NBX_OUT_ADD_F64) NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, s));
+        }
+        ctx->fault.ensure(2 * sizeof(unsigned long long));
+        NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 2 * sizeof(unsigned long long), s));
+        P.out_mode = out_mode;
+        P.out = dout;
+        P.fault = static_cast<unsigned long long*>(ctx->fault.p);
+        P.fault_bg = P.fault + 1;
+        NBX_CUDA(nbx::launch_background(P, s));
+        unsigned long long f[2] = {~0ull, ~0ull};
+        NBX_CUDA(cudaMemcpyAsync(f, ctx->fault.p, sizeof(f), cudaMemcpyDeviceToHost, s));
+        if (!out_on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        ctx->fault_stage = 1;
+        bad = f[1] == ~0ull ? -1 : (int64_t)f[1];
         return NBX_OK;
     });
     if (st != NBX_OK) return st;

@@ -41,6 +41,8 @@ __all__ = [
     "lattice_transform",
     "nanobragg_spots",
     "add_array",
+    "add_background",
+    "simulate_image",
     "add_noise",
     "poisson_host",
     "describe",
@@ -146,7 +148,8 @@ def _table_arrays(table) -> tuple[np.ndarray, np.ndarray]:
     return hkl, amp
 
 
-def describe(ctx, *, src_begin: int = 0, src_end: int = 0, norm: float = 0.0) -> N.Descriptor:
+def describe(ctx, *, src_begin: int = 0, src_end: int = 0, norm: float = 0.0, background=None,
+             thickness_factor: float = 1.0) -> N.Descriptor:
     """Flatten a SpotsContext into the C descriptor (what the kernel reads).
 
     Accepts this package's SpotsContext or the reference's own (duck typing:
@@ -175,6 +178,8 @@ def describe(ctx, *, src_begin: int = 0, src_end: int = 0, norm: float = 0.0) ->
         norm=norm,
         src_begin=src_begin,
         src_end=src_end,
+        background=background,
+        thickness_factor=thickness_factor,
     )
 
 
@@ -275,6 +280,65 @@ class SpotsPlan:
             self.close()
         except Exception:
             pass
+
+
+def _bg_descriptor(profile, panel, spectrum, thickness_factor: float) -> N.Descriptor:
+    """Descriptor carrying only what the background kernel reads."""
+    return N.Descriptor(
+        panels=_panels_of(panel), oversample=1, beam_direction=spectrum.beam_direction,
+        polarization_on=spectrum.polarization_on, wavelengths=spectrum.wavelengths, weights=spectrum.weights,
+        fluence=spectrum.fluence, r_e_sqr=R_E_SQR, bases=np.eye(3)[None], n_cells=(1, 1, 1),
+        hkl=np.zeros((0, 3), np.int32), amplitudes=np.zeros(0), default_f=0.0, background=profile,
+        thickness_factor=thickness_factor)
+
+
+def add_background(profile, panel, spectrum, thickness_factor: float, out: PixelBuffer, executor=None) -> None:
+    """Diffuse (air/water) background into ``out`` on the GPU (kernels.py:279-312).
+
+    out[p] = r_e^2 fluence thickness_factor / sum(w) * sum_w w f_bg(sin(theta)/lambda_w)^2 * Omega*pol,
+    at pixel centres.  f32 store (the reference) or f64 (extension).
+    """
+    _check_out(out, panel)
+    t0 = time.perf_counter()
+    desc = _bg_descriptor(profile, panel, spectrum, thickness_factor)
+    cx = N.context()
+    bad = N.C.c_int64(-1)
+    mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
+    status = cx.lib.nbx_background(cx.handle, N.C.byref(desc.c), mode, out.data.ctypes.data, 0, N.C.byref(bad))
+    N.check(cx, status, bad.value, label="add_background")
+    if executor is not None and hasattr(executor, "timing_log"):
+        from .execution import TimingRecord
+
+        executor.timing_log.append(TimingRecord("add_background", (time.perf_counter() - t0) * 1e3))
+
+
+def simulate_image(ctx, background=None, thickness_factor: float = 1.0, out: PixelBuffer | None = None,
+                   executor=None) -> PixelBuffer:
+    """One image's 64-bit accumulator, spots + background fused in ONE launch (scheduler.py:156-183).
+
+    Equals the reference pipeline bit for bit in structure: f64(f32(spots)) then
+    + f64(f32(background)) (add_array, kernels.py:315-331), with the spot and
+    background stages evaluated by the same kernel and no 32-bit staging
+    buffers in HBM.  ``background=None`` skips the background stage.
+    """
+    dims = ctx.panel.dims
+    if out is None:
+        out = PixelBuffer.zeros(dims, "f64")
+    _check_out(out, ctx.panel)
+    if out.precision != "f64":
+        raise ShapeMismatchError("simulate_image accumulates into an f64 buffer")
+    t0 = time.perf_counter()
+    desc = describe(ctx, background=background, thickness_factor=thickness_factor)
+    cx = N.context()
+    bad = N.C.c_int64(-1)
+    status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), N.COMPUTE[getattr(ctx, "compute", "fp64")],
+                              N.OUT_IMAGE_F64, out.data.ctypes.data, 0, N.C.byref(bad))
+    N.check(cx, status, bad.value, label="simulate_image")
+    if executor is not None and hasattr(executor, "timing_log"):
+        from .execution import TimingRecord
+
+        executor.timing_log.append(TimingRecord("simulate_image", (time.perf_counter() - t0) * 1e3))
+    return out
 
 
 def add_array(lhs: PixelBuffer, rhs: PixelBuffer, executor=None) -> None:

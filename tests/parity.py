@@ -80,3 +80,18 @@ def metrics(got: np.ndarray, ref: np.ndarray, dims) -> dict:
     pix_rel = float(np.max(np.abs(got[bright] - ref[bright]) / ref[bright])) if bright.any() else 0.0
     return {"total": float(tot), "spot": spot, "n_spots": int(n),
             "pix_abs_over_max": float(np.max(np.abs(got - ref)) / mx), "pix_rel_bright": pix_rel}
+
+
+def bg_inputs(case: dict):
+    """(profile, panel, spectrum, thickness_factor) of a background fixture."""
+    from paper_2205_07976_b200 import BackgroundProfile
+
+    p = case["panel"]
+    panel = DetectorPanel(int(p[0]), int(p[1]), float(p[2]), float(p[3]), (float(p[4]), float(p[5])),
+                          fast_axis=tuple(float(x) for x in case["fast_axis"]),
+                          slow_axis=tuple(float(x) for x in case["slow_axis"]))
+    beam = BeamSpectrum(samples=tuple(map(tuple, case["samples"].tolist())), fluence=float(case["fluence"]),
+                        polarization_on=bool(case["pol"]),
+                        beam_direction=tuple(float(x) for x in case["beam_dir"]))
+    prof = BackgroundProfile(points=tuple(map(tuple, case["bg_points"].tolist())))
+    return prof, panel, beam, float(case["thickness_factor"])

@@ -1,0 +1,74 @@
+"""GPU: add_background (the paper's second kernel) and the fused simulate_image accumulator."""
+import numpy as np
+import pytest
+
+import parity
+from oracle import oracle
+from paper_2205_07976_b200 import (
+    BackgroundProfile,
+    PatternFault,
+    PixelBuffer,
+    add_array,
+    add_background,
+    describe,
+    nanobragg_spots,
+    simulate_image,
+    synthetic,
+)
+from paper_2205_07976_b200.kernels import _bg_descriptor
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["bg_flat", "bg_scalar", "bg_water_80"])
+def test_background_matches_reference(gpu, name):
+    case = parity.load(name)
+    prof, panel, beam, tf = parity.bg_inputs(case)
+    out = PixelBuffer.zeros(panel.dims, "f64")
+    add_background(prof, panel, beam, tf, out)
+    np.testing.assert_allclose(out.data, case["ref_bg_f64"], rtol=1e-12, atol=0)
+    out32 = PixelBuffer.zeros(panel.dims, "f32")
+    add_background(prof, panel, beam, tf, out32)
+    rel = np.abs(out32.data.astype(np.float64) - case["ref_bg_f32"]) / case["ref_bg_f32"]
+    assert rel.max() <= 2.0 ** -23
+
+
+def test_simulate_image_matches_reference_pipeline(gpu):
+    """test_kernels.py:439-471 / test_acceptance.py:68-111: spots + background + add_array, 1e-6 rel per pixel."""
+    case = parity.load("pipeline_full")
+    prof, _, _, tf = parity.bg_inputs(case)
+    img = simulate_image(parity.context(case), background=prof, thickness_factor=tf)
+    rel = np.abs(img.data - case["ref_image"]) / np.abs(case["ref_image"])
+    assert rel.max() < 1e-6
+    # and it is exactly the staged pipeline: f64(f32 spots) + f64(f32 background)
+    spots = PixelBuffer.zeros((4, 4))
+    nanobragg_spots(parity.context(case), spots)
+    bg = PixelBuffer.zeros((4, 4))
+    add_background(prof, *parity.bg_inputs(case)[1:3], tf, bg)
+    acc = PixelBuffer.zeros((4, 4), "f64")
+    add_array(acc, spots)
+    add_array(acc, bg)
+    assert np.array_equal(img.data, acc.data)
+
+
+def test_simulate_image_ls49_roi_vs_oracle(gpu):
+    water = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.162, 8.0),
+                                      (0.3, 6.5)))
+    panel = synthetic.roi(synthetic.rayonix_panel(), 100, 3000, 16, 64)
+    for compute, tol in (("fp64", 1e-9), ("fp32", 1e-4)):
+        ctx = synthetic.ls49_context(panel=panel, n_channels=12, n_domains=3, compute=compute)
+        img = simulate_image(ctx, background=water, thickness_factor=0.7)
+        sp, _ = oracle.spots(describe(ctx), "f64")
+        bg, _ = oracle.background(_bg_descriptor(water, panel, ctx.spectrum, 0.7), "f64")
+        want = sp.astype(np.float32).astype(np.float64) + bg.astype(np.float32).astype(np.float64)
+        assert abs(img.data.sum() - want.sum()) / want.sum() < tol
+        no_bg = simulate_image(ctx)
+        assert np.allclose(no_bg.data, sp.astype(np.float32).astype(np.float64), rtol=tol)
+
+
+def test_background_fault_is_labelled(gpu):
+    case = parity.load("bg_scalar")
+    prof, panel, beam, tf = parity.bg_inputs(case)
+    with pytest.raises(PatternFault) as info:
+        add_background(prof, panel, beam, 1e300, PixelBuffer.zeros(panel.dims))
+    assert info.value.label == "add_background" and info.value.index == 0

@@ -94,3 +94,26 @@ def test_oracle_fault_pixel():
     desc.c.default_f = 1e30
     _, bad = oracle.spots(desc, "f32")
     assert bad == 0
+
+
+@pytest.mark.parametrize("name", ["bg_flat", "bg_scalar", "bg_water_80"])
+def test_oracle_background_matches_reference_fixture(name):
+    from paper_2205_07976_b200.kernels import _bg_descriptor
+
+    case = parity.load(name)
+    desc = _bg_descriptor(*parity.bg_inputs(case))
+    got, bad = oracle.background(desc, "f64")
+    assert bad == -1
+    np.testing.assert_allclose(got, case["ref_bg_f64"], rtol=1e-13, atol=0)
+    f32, _ = oracle.background(desc, "f32")
+    assert np.mean(f32 == case["ref_bg_f32"]) > 0.99
+
+
+def test_oracle_pipeline_matches_reference_fixture():
+    from paper_2205_07976_b200.kernels import _bg_descriptor
+
+    case = parity.load("pipeline_full")
+    spots, _ = oracle.spots(describe(parity.context(case)), "f32")
+    bg, _ = oracle.background(_bg_descriptor(*parity.bg_inputs(case)), "f32")
+    acc = spots.astype(np.float64) + bg.astype(np.float64)
+    np.testing.assert_allclose(acc, case["ref_image"], rtol=1e-7, atol=0)

@@ -84,6 +84,35 @@ def run_reference(case):
     return out32.data.copy(), cap
 
 
+def run_reference_bg(case):
+    """(ref_bg_f32, ref_bg_f64) from xtrace.kernels.add_background (kernels.py:279-312)."""
+    p = case["panel"]
+    panel = xm.DetectorPanel(int(p[0]), int(p[1]), float(p[2]), float(p[3]), (float(p[4]), float(p[5])),
+                             fast_axis=tuple(case["fast_axis"]), slow_axis=tuple(case["slow_axis"]))
+    beam = xm.BeamSpectrum(samples=tuple(map(tuple, case["samples"])), fluence=float(case["fluence"]),
+                           polarization_on=bool(case["pol"]), beam_direction=tuple(case["beam_dir"]))
+    prof = xm.BackgroundProfile(points=tuple(map(tuple, case["bg_points"])))
+    tf = float(case["thickness_factor"])
+    out32 = xk.PixelBuffer.zeros(panel.dims)
+    xk.add_background(prof, panel, beam, tf, out32)
+    cap = np.zeros(panel.n_pixels)
+    shim = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np) if not k.startswith("__")})
+    shim.float32 = np.float64
+    real_np, real_store = xk.np, xk._store_checked
+
+    def store(out_slice, values, lo):
+        cap[lo:lo + len(values)] = values
+        real_store(out_slice, values, lo)
+
+    xk.np, xk._store_checked = shim, store
+    try:
+        xk.add_background(prof, panel, beam, tf, xk.PixelBuffer.zeros(panel.dims))
+    finally:
+        xk.np, xk._store_checked = real_np, real_store
+    assert np.array_equal(cap.astype(np.float32), out32.data)
+    return out32.data.copy(), cap
+
+
 def base_case(**kw):
     c = dict(cell=(100.0, 100.0, 100.0, 90.0, 90.0, 90.0), orientation=np.eye(3), n_cells=(5, 5, 5),
              mosaic=np.eye(3)[None], hkl=np.zeros((0, 3), np.int32), amp=np.zeros(0), default_f=100.0,
@@ -151,10 +180,37 @@ CASES = {
 }
 
 
+WATER = np.array([[0.0, 2.57], [0.0365, 2.58], [0.07, 2.8], [0.12, 5.0], [0.162, 8.0], [0.3, 6.5]])
+BG_CASES = {
+    # test_kernels.py:249-260 flat profile, polarization off
+    "bg_flat": base_case(bg_points=np.array([[0.0, 3.0], [1.0, 3.0]]), thickness_factor=1.0),
+    # test_kernels.py:267-279
+    "bg_scalar": base_case(bg_points=np.array([[0.0, 10.0], [0.5, 2.0]]), thickness_factor=1.3, pol=True),
+    # test_kernels.py:281-293 (80x80, two wavelengths, water profile)
+    "bg_water_80": base_case(panel=(80, 80, 100e-6, 0.12, 39.5, 39.5), samples=np.array([[1.0, 0.7], [1.05, 0.3]]),
+                             pol=True, bg_points=WATER, thickness_factor=1.0),
+}
+
+
+def pipeline_case():
+    """test_kernels.py:439-471: spots + background -> f64 accumulator via add_array."""
+    case = base_case(mosaic=two_domain(), oversample=2, samples=np.array([[1.0, 0.6], [1.05, 0.4]]), pol=True,
+                     bg_points=WATER[:4], thickness_factor=1.0,
+                     **dict(zip(("hkl", "amp"), entries({(1, 0, 0): 250.0}))))
+    s32, _ = run_reference(case)
+    b32, _ = run_reference_bg(case)
+    acc = xk.PixelBuffer.zeros((4, 4), "f64")
+    xk.add_array(acc, xk.PixelBuffer((4, 4), "f32", s32))
+    xk.add_array(acc, xk.PixelBuffer((4, 4), "f32", b32))
+    return case, acc.data.copy()
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
     for name in names or CASES:
+        if name not in CASES:
+            continue
         case = CASES[name]
         t0 = time.perf_counter()
         f32, f64 = run_reference(case)
@@ -164,6 +220,20 @@ def main(names):
         meta[name] = {"pixels": int(f32.size), "ref_seconds": round(dt, 2), "total_f64": float(f64.sum()),
                       "max_f64": float(f64.max())}
         print(name, meta[name], flush=True)
+    for name in names or BG_CASES:
+        if name not in BG_CASES:
+            continue
+        case = BG_CASES[name]
+        f32, f64 = run_reference_bg(case)
+        np.savez_compressed(OUT / f"{name}.npz", ref_bg_f32=f32, ref_bg_f64=f64,
+                            **{k: np.asarray(v) for k, v in case.items()})
+        meta[name] = {"pixels": int(f32.size), "total_f64": float(f64.sum())}
+        print(name, meta[name], flush=True)
+    if not names or "pipeline_full" in names:
+        case, acc = pipeline_case()
+        np.savez_compressed(OUT / "pipeline_full.npz", ref_image=acc, **{k: np.asarray(v) for k, v in case.items()})
+        meta["pipeline_full"] = {"pixels": int(acc.size), "total": float(acc.sum())}
+        print("pipeline_full", meta["pipeline_full"], flush=True)
     old = json.loads((OUT / "index.json").read_text()) if (OUT / "index.json").exists() else {}
     old.update(meta)
     (OUT / "index.json").write_text(json.dumps(old, indent=1, sort_keys=True) + "\n")
