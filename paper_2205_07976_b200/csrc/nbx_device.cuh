@@ -197,3 +197,84 @@ __device__ __forceinline__ T shape_latt2(T hrad2, T nnn) {
 }
 
 }  // namespace nbx
+
+namespace nbx {
+
+// ---------------------------------------------------------------------------
+// Packed FP32 (sm_100a FFMA2 / FMUL2 / FADD2): two channels per thread in one
+// instruction.  The FMA pipe's FLOP rate is unchanged, but every packed op
+// takes ONE issue slot for two FMAs, and the FP32 spot loop is issue-bound.
+// lo half = channel w, hi half = channel w + 1.  Broadcast operands built with
+// bc2() compile to scalar-register operands (R.F32), costing no extra register.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2x;
+
+__device__ __forceinline__ f2x pk2(float lo, float hi) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f2x bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ float lo2(f2x v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a;
+}
+__device__ __forceinline__ float hi2(f2x v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return b;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+template <int DEG>
+__device__ __forceinline__ f2x q_sinpi_f32x2(f2x s) {
+    if constexpr (DEG == 3) {
+        f2x q = fma2(bc2(-0.1772475662559543266f), s, bc2(0.8095661799590536796f));
+        q = fma2(q, s, bc2(-1.644831841650291668f));
+        return fma2(q, s, bc2(1.0f));
+    } else {
+        f2x q = fma2(bc2(0.02460929274903431744f), s, bc2(-0.1903951449679496331f));
+        q = fma2(q, s, bc2(0.8117093632737977162f));
+        q = fma2(q, s, bc2(-1.644933097370079417f));
+        return fma2(q, s, bc2(1.0f));
+    }
+}
+
+struct AxisF32x2 {
+    f2x num, den, j, m;
+};
+
+// Unbiased (hot-loop) axis for two channels: the same arithmetic as axis_f32
+// without |t| (signs drop out of the squared ratio) and without the bias
+// (t == 0 -> 0/0 is caught by the caller's finiteness check).
+template <int DEG>
+__device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x magic) {
+    AxisF32x2 a;
+    const f2x M = bc2(kMagicF32), neg1 = bc2(-1.0f);
+    const f2x x = fma2(S, D, f0);
+    a.m = add2(x, magic);
+    a.j = fma2(magic, neg1, a.m);         // m - magic = rint(x), exact
+    const f2x t = fma2(a.j, neg1, x);     // x - j, exact
+    const f2x nk = fma2(fma2(N, t, M), neg1, M);  // -rint(N t)
+    const f2x r = fma2(N, t, nk);         // N t - rint(N t)
+    a.num = mul2(r, q_sinpi_f32x2<DEG>(mul2(r, r)));
+    a.den = mul2(t, q_sinpi_f32x2<DEG>(mul2(t, t)));
+    return a;
+}
+
+}  // namespace nbx

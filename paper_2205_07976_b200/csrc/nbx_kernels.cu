@@ -79,23 +79,26 @@ constexpr int kNewtonF64 = 1;
 // yields the analytic limit N.  Underflow of the three-axis products is
 // caught the same way.
 //
-// FP32 path: channels come in chunks with one FP64 phase anchor each; the
-// l-axis magic carries the chunk's cell so that the float built by the index
-// FMA chain is directly the biased cell number.
+// FP32 path: channels come in chunks with one FP64 phase anchor each, stored
+// as pairs {D_w, D_w+1, wt_w, wt_w+1} (odd chunks padded with a zero-weight
+// channel); the l-axis magic carries the chunk's cell so that the float built
+// by the index FMA chain is directly the biased cell number.
 // ---------------------------------------------------------------------------
+
+// Scalar form: the biased re-evaluation, the non-grating shapes, the WIDE index.
 template <int SHAPE, bool WIDE, int PDEG, bool BIAS>
-__device__ __forceinline__ float chunk_sum_f32(const SpotsParams& P, const float2* __restrict__ sch, int w0, int w1,
-                                               float a_hi, float b_hi, float c_hi, float fa, float fb, float fc,
-                                               float magic_c, const float* __restrict__ base) {
+__device__ __noinline__ float chunk_sum_f32_scalar(const SpotsParams& P, const float4* __restrict__ sch, int p0,
+                                                   int p1, float a_hi, float b_hi, float c_hi, float fa, float fb,
+                                                   float fc, float magic_c, const float* __restrict__ base) {
     const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
     const float sHf = (float)P.sH, sKf = (float)P.sK;
     float accf = 0.0f;
-#pragma unroll 4
-    for (int w = w0; w < w1; ++w) {
-        const float2 c = sch[w];
-        const AxisF32 A = axis_f32<PDEG, BIAS>(a_hi, c.x, fa, Na);
-        const AxisF32 B = axis_f32<PDEG, BIAS>(b_hi, c.x, fb, Nb);
-        const AxisF32 C = axis_f32<PDEG, BIAS>(c_hi, c.x, fc, Nc, magic_c);
+    for (int q = 2 * p0; q < 2 * p1; ++q) {
+        const float4 c4 = sch[q >> 1];
+        const float D = (q & 1) ? c4.y : c4.x, wt = (q & 1) ? c4.w : c4.z;
+        const AxisF32 A = axis_f32<PDEG, BIAS>(a_hi, D, fa, Na);
+        const AxisF32 B = axis_f32<PDEG, BIAS>(b_hi, D, fb, Nb);
+        const AxisF32 C = axis_f32<PDEG, BIAS>(c_hi, D, fc, Nc, magic_c);
         float L2;
         if constexpr (SHAPE == 0) {
             const float nn = (A.num * B.num) * C.num;
@@ -108,22 +111,50 @@ __device__ __forceinline__ float chunk_sum_f32(const SpotsParams& P, const float
         }
         float F2;
         if constexpr (!WIDE) {
-            // M + cell0 + (jA sH + jB sK + jC), exact in the FP32 significand;
-            // its bit pattern minus 0x4B400000 is the cell (base is biased by that)
             const float fi = __fmaf_rn(A.j, sHf, __fmaf_rn(B.j, sKf, C.m));
             F2 = __ldg(base + __float_as_uint(fi));
         } else {
             const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
             F2 = __ldg(base + off);
         }
-        accf = __fmaf_rn(F2 * c.y, L2, accf);
+        accf = __fmaf_rn(F2 * wt, L2, accf);
     }
     return accf;
 }
 
+// Packed form (the hot loop): two channels per FFMA2/FMUL2/FADD2.  The two
+// halves are summed separately and combined at the end of the chunk.
+template <int PDEG>
+__device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const float4* __restrict__ sch, int p0, int p1,
+                                                 float a_hi, float b_hi, float c_hi, float fa, float fb, float fc,
+                                                 float magic_c, const float* __restrict__ base) {
+    const f2x Sa = bc2(a_hi), Sb = bc2(b_hi), Sc = bc2(c_hi);
+    const f2x Fa = bc2(fa), Fb = bc2(fb), Fc = bc2(fc);
+    const f2x Na = bc2(P.n_cells_f[0]), Nb = bc2(P.n_cells_f[1]), Nc = bc2(P.n_cells_f[2]);
+    const f2x M = bc2(kMagicF32), Mc = bc2(magic_c);
+    const f2x sH = bc2((float)P.sH), sK = bc2((float)P.sK);
+    f2x acc = bc2(0.0f);
+#pragma unroll 2
+    for (int q = p0; q < p1; ++q) {
+        const float4 c4 = sch[q];
+        const f2x D = pk2(c4.x, c4.y), W = pk2(c4.z, c4.w);
+        const AxisF32x2 A = axis_f32x2<PDEG>(Sa, D, Fa, Na, M);
+        const AxisF32x2 B = axis_f32x2<PDEG>(Sb, D, Fb, Nb, M);
+        const AxisF32x2 C = axis_f32x2<PDEG>(Sc, D, Fc, Nc, Mc);
+        const f2x nn = mul2(mul2(A.num, B.num), C.num);
+        const f2x dd = mul2(mul2(A.den, B.den), C.den);
+        const f2x ratio = mul2(nn, pk2(rcp_approx_f32(lo2(dd)), rcp_approx_f32(hi2(dd))));
+        const f2x L2 = mul2(ratio, ratio);
+        const f2x fi = fma2(A.j, sH, fma2(B.j, sK, C.m));  // biased cell numbers (see scalar form)
+        const f2x F2 = pk2(__ldg(base + __float_as_uint(lo2(fi))), __ldg(base + __float_as_uint(hi2(fi))));
+        acc = fma2(mul2(F2, W), L2, acc);
+    }
+    return lo2(acc) + hi2(acc);
+}
+
 template <int SHAPE, bool WIDE, int PDEG>
 __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const ChunkF32* __restrict__ sck,
-                                                 const float2* __restrict__ sch, double Sa, double Sb,
+                                                 const float4* __restrict__ sch, double Sa, double Sb,
                                                  double Sc) {
     const float a_hi = __double2float_rn(Sa), b_hi = __double2float_rn(Sb), c_hi = __double2float_rn(Sc);
     double dacc = 0.0;
@@ -140,12 +171,17 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         // WIDE: per-chunk base + integer offset
         const float magic_c = WIDE ? kMagicF32 : kMagicF32 + (float)cell0;
         const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : -(int64_t)0x4B400000);
-        float accf = chunk_sum_f32<SHAPE, WIDE, PDEG, false>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb,
-                                                             fc, magic_c, base);
+        float accf;
+        if constexpr (SHAPE == 0 && !WIDE) {
+            accf = chunk_sum_f32x2<PDEG>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb, fc, magic_c, base);
+        } else {
+            accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, false>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa,
+                                                                  fb, fc, magic_c, base);
+        }
         if constexpr (SHAPE == 0) {
             if (!isfinite(accf))  // exact Bragg position / underflow: the reference's limit branch
-                accf = chunk_sum_f32<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb,
-                                                              fc, magic_c, base);
+                accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi,
+                                                                     fa, fb, fc, magic_c, base);
         }
         dacc += (double)accf;
     }
@@ -203,9 +239,9 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, 3) spots_kernel(const SpotsP
     if constexpr (COMPUTE == 1) {
         ChunkF32* k = reinterpret_cast<ChunkF32*>(smem_raw);
         for (int i = tid; i < P.n_chunks; i += kBlockX * kBlockY) k[i] = P.chunks[i];
-        float2* s = reinterpret_cast<float2*>(smem_raw + 16 * P.n_chunks);
-        const float2* g = static_cast<const float2*>(P.chan);
-        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
+        float4* s = reinterpret_cast<float4*>(smem_raw + 16 * P.n_chunks);
+        const float4* g = static_cast<const float4*>(P.chan);
+        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];  // FP32: n_src counts pairs
     } else {
         double2* s = reinterpret_cast<double2*>(smem_raw);
         const double2* g = static_cast<const double2*>(P.chan);
@@ -265,7 +301,7 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, 3) spots_kernel(const SpotsP
                     if constexpr (COMPUTE == 1) {
                         sub += domain_sum_f32<SHAPE, WIDE, PDEG>(
                             P, reinterpret_cast<const ChunkF32*>(smem_raw),
-                            reinterpret_cast<const float2*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
+                            reinterpret_cast<const float4*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
                     } else {
                         sub += domain_sum_f64<SHAPE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
                     }
@@ -404,7 +440,7 @@ cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide
         const size_t smem = (size_t)P.n_src * 16;
         return launch_shape<0, false>(P, shape, smem, st);
     }
-    const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 8;
+    const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 16;  // n_src = channel pairs
     if (compute == 2 && shape == 0)
         return wide ? launch_t<1, 0, true, 4>(P, smem, st) : launch_t<1, 0, false, 4>(P, smem, st);
     return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);

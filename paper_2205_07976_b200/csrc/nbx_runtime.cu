@@ -389,6 +389,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         plan->out_scale = plan->scale / sigma;
 
         // channels
+        int n_chan_entries = n_src;  // FP64: channels; FP32: channel pairs
         if (compute == NBX_COMPUTE_FP32) {
             // sort by 1/lambda and cut chunks whose phase offsets stay small:
             // |S (iv - iv0)| <= smax (max - min) / 2 <= 1 -> |x| <= 1.5 in the kernel
@@ -399,20 +400,28 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 iv[i] = 1.0 / d->wavelengths[sb + i];  // kernels.py:257
             }
             std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return iv[x] < iv[y]; });
+            // pairs {D_w, D_w+1, wt_w, wt_w+1} for the packed (f32x2) loop; an odd
+            // chunk is padded with a zero-weight copy of its last channel
             std::vector<nbx::ChunkF32> chunks;
-            std::vector<float> ch(2 * (size_t)n_src);
-            int i0 = 0;
+            std::vector<float> ch;
+            int i0 = 0, npairs = 0;
             while (i0 < n_src) {
                 int i1 = i0 + 1;
                 while (i1 < n_src && i1 - i0 < 64 && (iv[order[i1]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++i1;
                 const double iv0 = 0.5 * (iv[order[i0]] + iv[order[i1 - 1]]);
-                chunks.push_back(nbx::ChunkF32{iv0, i0, i1});
-                for (int q = i0; q < i1; ++q) {
-                    ch[2 * q + 0] = (float)(iv[order[q]] - iv0);
-                    ch[2 * q + 1] = (float)d->weights[sb + order[q]];
+                const int p0 = npairs;
+                for (int q = i0; q < i1; q += 2) {
+                    const int q1 = q + 1 < i1 ? q + 1 : q;
+                    ch.push_back((float)(iv[order[q]] - iv0));
+                    ch.push_back((float)(iv[order[q1]] - iv0));
+                    ch.push_back((float)d->weights[sb + order[q]]);
+                    ch.push_back(q + 1 < i1 ? (float)d->weights[sb + order[q1]] : 0.0f);
+                    ++npairs;
                 }
+                chunks.push_back(nbx::ChunkF32{iv0, p0, npairs});
                 i0 = i1;
             }
+            n_chan_entries = npairs;
             plan->chan.ensure(ch.size() * sizeof(float));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(float), cudaMemcpyHostToDevice));
             plan->chunks.ensure(chunks.size() * sizeof(nbx::ChunkF32));
@@ -448,7 +457,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         P.oversample = os;
         P.bases = static_cast<const double*>(plan->bases.p);
         P.n_dom = d->n_domains;
-        P.n_src = n_src;
+        P.n_src = n_chan_entries;
         P.chan = plan->chan.p;
         for (int a = 0; a < 3; ++a) {
             P.beam[a] = d->beam_direction[a];
