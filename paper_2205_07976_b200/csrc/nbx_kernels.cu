@@ -64,6 +64,12 @@ __device__ __forceinline__ double background_value(const SpotsParams& P, const D
     return P.bg_scale * acc * op;
 }
 
+#ifndef NBX_MIN_BLOCKS_F32
+#define NBX_MIN_BLOCKS_F32 3  // 80 registers: the packed FP32 loop spills at 64
+#endif
+#ifndef NBX_MIN_BLOCKS_F64
+#define NBX_MIN_BLOCKS_F64 4  // 64 registers, no spills: 50% occupancy for the FP64 pipe
+#endif
 constexpr int kBlockX = 32;
 constexpr int kBlockY = 8;
 constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
@@ -111,8 +117,9 @@ __device__ __noinline__ float chunk_sum_f32_scalar(const SpotsParams& P, const f
         }
         float F2;
         if constexpr (!WIDE) {
-            const float fi = __fmaf_rn(A.j, sHf, __fmaf_rn(B.j, sKf, C.m));
-            F2 = __ldg(base + __float_as_uint(fi));
+            const uint32_t cell = (__float_as_uint(A.m) << P.sh_h) + (__float_as_uint(B.m) << P.sh_k) +
+                                  __float_as_uint(C.m);
+            F2 = __ldg(base + cell);
         } else {
             const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
             F2 = __ldg(base + off);
@@ -145,8 +152,12 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
         const f2x dd = mul2(mul2(A.den, B.den), C.den);
         const f2x ratio = mul2(nn, pk2(rcp_approx_f32(lo2(dd)), rcp_approx_f32(hi2(dd))));
         const f2x L2 = mul2(ratio, ratio);
-        const f2x fi = fma2(A.j, sH, fma2(B.j, sK, C.m));  // biased cell numbers (see scalar form)
-        const f2x F2 = pk2(__ldg(base + __float_as_uint(lo2(fi))), __ldg(base + __float_as_uint(hi2(fi))));
+        // cell + lea_bias from the magic-rounded bit patterns: two shift-adds on the ALU per half
+        const uint32_t c0 = (__float_as_uint(lo2(A.m)) << P.sh_h) + (__float_as_uint(lo2(B.m)) << P.sh_k) +
+                            __float_as_uint(lo2(C.m));
+        const uint32_t c1 = (__float_as_uint(hi2(A.m)) << P.sh_h) + (__float_as_uint(hi2(B.m)) << P.sh_k) +
+                            __float_as_uint(hi2(C.m));
+        const f2x F2 = pk2(__ldg(base + c0), __ldg(base + c1));
         acc = fma2(mul2(F2, W), L2, acc);
     }
     return lo2(acc) + hi2(acc);
@@ -170,7 +181,7 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         // !WIDE: the l-axis magic carries cell0 and base absorbs the float bias;
         // WIDE: per-chunk base + integer offset
         const float magic_c = WIDE ? kMagicF32 : kMagicF32 + (float)cell0;
-        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : -(int64_t)0x4B400000);
+        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : -(int64_t)P.lea_bias);
         float accf;
         if constexpr (SHAPE == 0 && !WIDE) {
             accf = chunk_sum_f32x2<PDEG>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb, fc, magic_c, base);
@@ -233,7 +244,7 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 // The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path.
 // ---------------------------------------------------------------------------
 template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
-__global__ void __launch_bounds__(kBlockX* kBlockY, 3) spots_kernel(const SpotsParams P) {
+__global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : NBX_MIN_BLOCKS_F64) spots_kernel(const SpotsParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.y * kBlockX + threadIdx.x;
     if constexpr (COMPUTE == 1) {

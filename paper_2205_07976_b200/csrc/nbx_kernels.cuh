@@ -55,7 +55,8 @@ struct SpotsParams {
     // dense-grid index: idx = (n_h - lo_h) * sH + (n_k - lo_k) * sK + (n_l - lo_l)
     int32_t lo[3];
     int32_t sH, sK;
-    float pad2;
+    int32_t sh_h, sh_k;            // FP32: log2 of the power-of-two strides
+    uint32_t lea_bias;             // FP32: 0x4B400000 (sH + sK + 1) mod 2^32
     double out_scale;              // r_e^2 fluence / norm (/ sigma on the FP32 path)
     void* out;
     unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none

@@ -355,16 +355,39 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         for (int a = 0; a < 3; ++a) P.lo[a] = -hmax[a];
         P.sK = (int32_t)dims[2];
         P.sH = (int32_t)(dims[1] * dims[2]);
-        // FP32 magic index: every cell + offset (|j| <= 2) must stay inside the 2^22 window
-        const bool wide32 = cells + 2 * ((int64_t)P.sH + P.sK + 1) >= (int64_t(1) << 22);
-        plan->wide = (compute == NBX_COMPUTE_FP32) ? wide32 : false;
+        int64_t cells_alloc = cells;
+        plan->wide = false;
+        if (compute == NBX_COMPUTE_FP32) {
+            // FP32 index: power-of-two strides so that the cell number is two shift-adds
+            // of the magic-rounded floats' bit patterns (ALU pipe, no FMA-pipe work):
+            //   bits(mA) << lg(sH) + bits(mB) << lg(sK) + bits(mC) = cell + c (mod 2^32),
+            // c = 0x4B400000 (sH + sK + 1) mod 2^32 absorbed by the base pointer.
+            // Needs every cell + offset (|j| <= 2) inside the 2^22 magic window and no
+            // 2^32 wrap; otherwise the WIDE (integer-conversion) index is used.
+            int lk = 0, lh = 0;
+            while ((int64_t(1) << lk) < dims[2]) ++lk;
+            while ((int64_t(1) << lh) < dims[1]) ++lh;
+            const int64_t sK2 = int64_t(1) << lk, sH2 = int64_t(1) << (lk + lh);
+            const int64_t alloc2 = dims[0] * sH2;
+            const uint64_t c = (uint64_t(0x4B400000u) * (uint64_t)(sH2 + sK2 + 1)) & 0xFFFFFFFFull;
+            if (alloc2 + 2 * (sH2 + sK2 + 1) < (int64_t(1) << 22) && c + (uint64_t)alloc2 < (uint64_t(1) << 32)) {
+                P.sK = (int32_t)sK2;
+                P.sH = (int32_t)sH2;
+                P.sh_k = lk;
+                P.sh_h = lk + lh;
+                P.lea_bias = (uint32_t)c;
+                cells_alloc = alloc2;
+            } else {
+                plan->wide = true;
+            }
+        }
         double smax = 0.0;  // largest |rel . a| over domains and axes (Angstrom)
         for (int dd = 0; dd < d->n_domains; ++dd)
             for (int a = 0; a < 3; ++a) smax = std::max(smax, norm3(d->bases + 9 * dd + 3 * a) * relmax);
 
         // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma)
         const double def2 = d->default_f * d->default_f;
-        std::vector<double> f2(cells, def2);
+        std::vector<double> f2(cells_alloc, def2);
         double maxf2 = def2;
         for (int i = 0; i < d->n_entries; ++i) {
             const int h = d->hkl[3 * i], k = d->hkl[3 * i + 1], l = d->hkl[3 * i + 2];
@@ -429,10 +452,10 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                                 cudaMemcpyHostToDevice));
             P.chunks = static_cast<const nbx::ChunkF32*>(plan->chunks.p);
             P.n_chunks = (int32_t)chunks.size();
-            std::vector<float> tf(cells);
-            for (int64_t i = 0; i < cells; ++i) tf[i] = (float)(f2[i] * sigma);
-            plan->table.ensure(cells * sizeof(float));
-            NBX_CUDA(cudaMemcpy(plan->table.p, tf.data(), cells * sizeof(float), cudaMemcpyHostToDevice));
+            std::vector<float> tf(cells_alloc);
+            for (int64_t i = 0; i < cells_alloc; ++i) tf[i] = (float)(f2[i] * sigma);
+            plan->table.ensure(cells_alloc * sizeof(float));
+            NBX_CUDA(cudaMemcpy(plan->table.p, tf.data(), cells_alloc * sizeof(float), cudaMemcpyHostToDevice));
         } else {
             std::vector<double> ch(2 * (size_t)n_src);
             for (int i = 0; i < n_src; ++i) {
@@ -476,7 +499,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         nbx_plan_info_t& I = plan->info;
         I.n_pixels = plan->n_pixels;
         I.steps = plan->steps;
-        I.table_cells = cells;
+        I.table_cells = cells_alloc;
         for (int a = 0; a < 3; ++a) {
             I.table_lo[a] = P.lo[a];
             I.table_dim[a] = (int32_t)dims[a];

@@ -18,6 +18,10 @@ for line in body.splitlines():
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
     if m:
         ins.append((int(m.group(1), 16), m.group(2).strip()))
+need = "LDS"
+if "--need" in sys.argv:
+    need = sys.argv[sys.argv.index("--need") + 1]
+    del sys.argv[sys.argv.index("--need"):sys.argv.index("--need") + 2]
 if len(sys.argv) >= 5:
     lo, hi = int(sys.argv[3], 16), int(sys.argv[4], 16)
 else:
@@ -28,7 +32,7 @@ else:
             tgt = int(m.group(1), 16)
             if tgt < addr:
                 seg = [t for a, t in ins if tgt <= a <= addr]
-                if any("LDS" in t for t in seg) and len(seg) > 40 and (best is None or len(seg) < best[2]):
+                if any(need in t for t in seg) and len(seg) > 40 and (best is None or len(seg) < best[2]):
                     best = (tgt, addr, len(seg))
     lo, hi = best[0], best[1]
 seg = [t for a, t in ins if lo <= a <= hi]
