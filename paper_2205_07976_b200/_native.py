@@ -15,7 +15,7 @@ import numpy as np
 
 from .errors import NativeError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libnbx.so"
+LIB_PATH = Path(os.environ.get("NBX_LIB") or Path(__file__).resolve().parent / "_lib" / "libnbx.so")
 
 NBX_OK, NBX_ERR_ARG, NBX_ERR_NUMERICAL, NBX_ERR_CUDA = 0, 1, 2, 3
 COMPUTE = {"fp64": 0, "fp32": 1}

@@ -44,32 +44,38 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the sources and link libnbx.so; returns its path."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile the sources and link libnbx.so; returns its path.
+
+    ``extra_flags``/``out`` build an experimental variant (e.g. -DNBX_MIN_BLOCKS_F32=4) elsewhere.
+    """
+    lib = Path(out) if out else LIB
+    if not force and out is None and not _stale():
         return LIB
+    lib.parent.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(exist_ok=True)
     objs = []
     logs = []
     for src in SOURCES:
-        obj = LIBDIR / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-dc" if False else "-c",
+        obj = lib.parent / (lib.stem + "_" + Path(src).stem + ".o")
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *(extra_flags or []), "-I", str(ROOT / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(res.stderr)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stderr}")
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    (LIBDIR / "ptxas.log").write_text("\n".join(logs))
+    os.replace(tmp, lib)
+    (lib.parent / (lib.stem + "_ptxas.log" if out else "ptxas.log")).write_text("\n".join(logs))
     if verbose:
         sys.stdout.write("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

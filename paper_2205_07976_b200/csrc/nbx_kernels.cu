@@ -65,10 +65,18 @@ __device__ __forceinline__ double background_value(const SpotsParams& P, const D
 }
 
 #ifndef NBX_MIN_BLOCKS_F32
-#define NBX_MIN_BLOCKS_F32 3  // 80 registers: the packed FP32 loop spills at 64
+#define NBX_MIN_BLOCKS_F32 2  // 128 registers for the 4x-unrolled packed loop
 #endif
+#ifndef NBX_PAIR_UNROLL
+#define NBX_PAIR_UNROLL 4  // measured best with 2 blocks / 128 registers (more ILP beats occupancy)
+#endif
+#ifndef NBX_F64_UNROLL
+#define NBX_F64_UNROLL 4  // measured best with 2 blocks (ILP beats occupancy, as on FP32)
+#endif
+constexpr int kF64Unroll = NBX_F64_UNROLL;
+constexpr int kPairUnroll = NBX_PAIR_UNROLL;  // channel pairs per FP32 loop iteration
 #ifndef NBX_MIN_BLOCKS_F64
-#define NBX_MIN_BLOCKS_F64 4  // 64 registers, no spills: 50% occupancy for the FP64 pipe
+#define NBX_MIN_BLOCKS_F64 2
 #endif
 constexpr int kBlockX = 32;
 constexpr int kBlockY = 8;
@@ -141,7 +149,7 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
     const f2x M = bc2(kMagicF32), Mc = bc2(magic_c);
     const f2x sH = bc2((float)P.sH), sK = bc2((float)P.sK);
     f2x acc = bc2(0.0f);
-#pragma unroll 2
+#pragma unroll kPairUnroll
     for (int q = p0; q < p1; ++q) {
         const float4 c4 = sch[q];
         const f2x D = pk2(c4.x, c4.y), W = pk2(c4.z, c4.w);
@@ -206,7 +214,7 @@ __device__ __forceinline__ double channel_sum_f64(const SpotsParams& P, const do
     const double* __restrict__ tab = static_cast<const double*>(P.table);
     const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
     double acc = 0.0;
-#pragma unroll 2
+#pragma unroll kF64Unroll
     for (int w = 0; w < P.n_src; ++w) {
         const double2 c = sch[w];
         const AxisF64 A = axis_f64<kPolyF64, BIAS>(Sa, c.x, Na);
