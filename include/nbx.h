@@ -53,9 +53,10 @@ enum {
     NBX_OUT_ADD_F64 = 2, /* out[p] += f64(f32(scale*acc)): spots fused with add_array
                             (kernels.py:315-331, scheduler.py:169-174) */
     NBX_OUT_RAW_F64 = 3, /* out[p] += acc (unscaled FP64 partial, for channel shards) */
-    NBX_OUT_IMAGE_F64 = 4 /* out[p] = f64(f32(spots)) + f64(f32(background)): the simulate_image
-                             accumulator (scheduler.py:156-183) in one launch; background only when
-                             the descriptor carries a profile (bg_points > 0) */
+    NBX_OUT_IMAGE_F64 = 4, /* out[p] = f64(f32(spots)) + f64(f32(background)): the simulate_image
+                              accumulator (scheduler.py:156-183) in one launch; background only when
+                              the descriptor carries a profile (bg_points > 0) */
+    NBX_OUT_IMAGE_F32 = 5  /* out[p] = f32(IMAGE_F64 value): the write_image payload (io.py:403-434) */
 };
 
 /* Lattice shape transforms.  SINCG is the reference's grating
@@ -158,7 +159,8 @@ int nbx_spots(void* ctx, const nbx_spots_desc* d, int compute, int out_mode,
               void* out, int out_on_device, int64_t* first_bad);
 /* With NBX_OUT_IMAGE_F64 a fault can come from either stage: *first_bad is the
  * spot stage's lowest bad pixel if any, else the background's, and
- * nbx_fault_stage(ctx) says which (0 spots, 1 background). */
+ * nbx_fault_stage(ctx) says which (0 spots, 1 background, 2 the f32 downcast of
+ * NBX_OUT_IMAGE_F32, i.e. write_image's refusal, io.py:409-411). */
 int nbx_fault_stage(void* ctx);
 
 /* Batch of independent images (SURVEY §8 E1 image sharding, config C3):
@@ -175,6 +177,27 @@ int nbx_plan_info(void* plan, nbx_plan_info_t* info);
 /* Device-time of the last nbx_plan_run spot kernel (ms, CUDA events). */
 double nbx_plan_last_kernel_ms(void* plan);
 void nbx_plan_destroy(void* plan);
+
+/* Pipelined image campaign (run_campaign/_rank_task, scheduler.py:190-247,
+ * write_image io.py:403-434): image i of descs is rendered as NBX_OUT_IMAGE_F32 and its raw
+ * little-endian float32 payload written to paths[i]; crcs[i] receives zlib.crc32 of the payload
+ * (the caller writes the JSON sidecar).  The kernel of image i+1 runs while image i is copied
+ * to the host, checksummed and written.  On a fault, *first_bad = (image << 40) | pixel and the
+ * images after it are not written. */
+int nbx_campaign(void* ctx, const nbx_spots_desc* descs, int n_images, int compute,
+                 const char* const* paths, uint32_t* crcs, int64_t* first_bad);
+
+/* Image statistics over n values (dtype 0 f32, 1 f64): out = {min, max, mean, total},
+ * deterministic fixed-tree sum (image_stats, kernels.py:346-371).  n >= 1. */
+int nbx_image_stats(void* ctx, const void* data, int64_t n, int dtype, int on_device, double* out4);
+
+/* Histogram (image_histogram, kernels.py:386-430): counts[n_bins] for [lo, hi] with the top
+ * bin closed, plus underflow / overflow.  The cumulative counts are the caller's prefix sum. */
+int nbx_image_histogram(void* ctx, const void* data, int64_t n, int dtype, int on_device, int n_bins,
+                        double lo, double hi, int64_t* counts, int64_t* underflow, int64_t* overflow);
+
+/* zlib-compatible CRC-32 (crc32(crc, data, n)); crc = 0 to start. */
+uint32_t nbx_crc32(uint32_t crc, const void* data, int64_t n);
 
 /* Diffuse background image alone -- add_background(profile, panel, spectrum,
  * thickness_factor, out) (kernels.py:279-312): pixel centres, one interpolated

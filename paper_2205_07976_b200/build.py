@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libnbx.so"
-SOURCES = ["nbx_kernels.cu", "nbx_runtime.cu"]
+SOURCES = ["nbx_kernels.cu", "nbx_reduce.cu", "nbx_runtime.cu"]
 HEADERS = ["nbx_device.cuh", "nbx_kernels.cuh", "nbx_poisson.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -198,6 +198,10 @@ __device__ __forceinline__ T shape_latt2(T hrad2, T nnn) {
 
 }  // namespace nbx
 
+#ifndef NBX_K_FRND
+#define NBX_K_FRND 0
+#endif
+
 namespace nbx {
 
 // ---------------------------------------------------------------------------
@@ -270,8 +274,14 @@ __device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x
     a.m = add2(x, magic);
     a.j = fma2(magic, neg1, a.m);         // m - magic = rint(x), exact
     const f2x t = fma2(a.j, neg1, x);     // x - j, exact
+#if NBX_K_FRND
+    // k = rint(N t) on the XU pipe (FRND), which the FP32 loop leaves mostly idle
+    const f2x u = mul2(N, t);
+    const f2x r = fma2(N, t, pk2(-rintf(lo2(u)), -rintf(hi2(u))));  // N t - k, one rounding
+#else
     const f2x nk = fma2(fma2(N, t, M), neg1, M);  // -rint(N t)
     const f2x r = fma2(N, t, nk);         // N t - rint(N t)
+#endif
     a.num = mul2(r, q_sinpi_f32x2<DEG>(mul2(r, r)));
     a.den = mul2(t, q_sinpi_f32x2<DEG>(mul2(t, t)));
     return a;

@@ -18,7 +18,7 @@
 
 namespace nbx {
 
-enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 4 };
+enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 4, kOutImageF32 = 5 };
 
 // ---------------------------------------------------------------------------
 // Diffuse background of one pixel (kernels.py:279-312): pixel-centre geometry
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
             static_cast<double*>(P.out)[p] += acc;
             break;
         }
-        default: {  // kOutImageF64: simulate_image's accumulator, spots (+ background) fused
+        default: {  // kOutImageF64/F32: simulate_image's accumulator, spots (+ background) fused
             const float v = (float)(P.out_scale * acc);
             bad = !isfinite(v);
             double img = (double)v;
@@ -366,7 +366,13 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
                 if (!isfinite(b)) atomicMin(P.fault_bg, (unsigned long long)p);
                 img += (double)b;
             }
-            static_cast<double*>(P.out)[p] = img;
+            if (P.out_mode == kOutImageF64) {
+                static_cast<double*>(P.out)[p] = img;
+            } else {  // write_image payload: the accumulator rounded to float32
+                const float o = (float)img;
+                static_cast<float*>(P.out)[p] = o;
+                if (!isfinite(o)) atomicMin(P.fault_bg + 1, (unsigned long long)p);
+            }
             break;
         }
     }

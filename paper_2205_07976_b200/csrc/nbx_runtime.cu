@@ -31,6 +31,10 @@ cudaError_t launch_noise(const void* mean, void* out, int64_t n, int dtype, uint
                          cudaStream_t st);
 cudaError_t launch_fma_probe(int fp64, void* out, int iters, int blocks, cudaStream_t st);
 cudaError_t launch_background(const SpotsParams& P, cudaStream_t st);
+cudaError_t launch_stats(const void* data, int64_t n, int dtype, void* parts, double* out, cudaStream_t st);
+size_t stats_scratch_bytes(int64_t n);
+cudaError_t launch_histogram(const void* data, int64_t n, int dtype, int n_bins, double lo, double hi,
+                             unsigned long long* counts, cudaStream_t st);
 }  // namespace nbx
 
 namespace {
@@ -74,7 +78,13 @@ struct Plan;
 
 struct Ctx {
     int device = 0;
-    int fault_stage = 0;      // stage of the last reported fault: 0 spots, 1 background
+    int fault_stage = 0;      // stage of the last reported fault: 0 spots, 1 background, 2 downcast
+    // campaign pipeline: second stream (device-to-host copies) and double buffers
+    cudaStream_t copy_stream = nullptr;
+    Plan* camp_plan[2] = {nullptr, nullptr};
+    DevBuf camp_out[2], camp_fault[2];
+    void* camp_host[2] = {nullptr, nullptr};
+    size_t camp_host_bytes = 0;
     Plan* oneshot = nullptr;  // device buffers reused by nbx_spots (cudaFree can stall for ~100 ms)
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
@@ -514,10 +524,36 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
     }
 }
 
-size_t out_elem_bytes(int mode) { return mode == NBX_OUT_F32 ? 4 : 8; }  // F64 / ADD / RAW / IMAGE: f64
+size_t out_elem_bytes(int mode) {
+    return (mode == NBX_OUT_F32 || mode == NBX_OUT_IMAGE_F32) ? 4 : 8;  // F64 / ADD / RAW / IMAGE_F64: f64
+}
 
 void check_mode(int mode) {
-    if (mode < NBX_OUT_F32 || mode > NBX_OUT_IMAGE_F64) throw ArgError("unknown output mode");
+    if (mode < NBX_OUT_F32 || mode > NBX_OUT_IMAGE_F32) throw ArgError("unknown output mode");
+}
+
+// Three fault slots per launch: spots, background, f32 downcast of the image.
+constexpr int kFaultSlots = 3;
+
+int64_t pick_fault(Ctx* ctx, const unsigned long long* fault) {
+    for (int s = 0; s < kFaultSlots; ++s) {
+        if (fault[s] != ~0ull) {
+            ctx->fault_stage = s;
+            return (int64_t)fault[s];
+        }
+    }
+    return -1;
+}
+
+// Enqueue one spot launch of `plan` into device buffer `dout` with fault slots `fault`.
+void enqueue_plan(Plan* plan, int mode, void* dout, unsigned long long* fault, cudaStream_t st) {
+    NBX_CUDA(cudaMemsetAsync(fault, 0xFF, kFaultSlots * sizeof(unsigned long long), st));
+    nbx::SpotsParams P = plan->P;
+    P.out_mode = mode;
+    P.out = dout;
+    P.fault = fault;
+    P.fault_bg = fault + 1;  // fault_bg[1] = the downcast slot
+    NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
 }
 
 // Run a plan into `out`; returns the lowest non-finite pixel or -1.
@@ -535,25 +571,49 @@ int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
         if (mode == NBX_OUT_ADD_F64 || mode == NBX_OUT_RAW_F64)
             NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, st));
     }
-    ctx->fault.ensure(2 * sizeof(unsigned long long));
-    NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 2 * sizeof(unsigned long long), st));
-    nbx::SpotsParams P = plan->P;
-    P.out_mode = mode;
-    P.out = dout;
-    P.fault = static_cast<unsigned long long*>(ctx->fault.p);
-    P.fault_bg = P.fault + 1;
+    ctx->fault.ensure(kFaultSlots * sizeof(unsigned long long));
+    unsigned long long* dfault = static_cast<unsigned long long*>(ctx->fault.p);
     NBX_CUDA(cudaEventRecord(ctx->ev0, st));
-    NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
+    enqueue_plan(plan, mode, dout, dfault, st);
     NBX_CUDA(cudaEventRecord(ctx->ev1, st));
     plan->timed = true;
-    unsigned long long fault[2] = {~0ull, ~0ull};
-    NBX_CUDA(cudaMemcpyAsync(fault, ctx->fault.p, sizeof(fault), cudaMemcpyDeviceToHost, st));
+    unsigned long long fault[kFaultSlots] = {~0ull, ~0ull, ~0ull};
+    NBX_CUDA(cudaMemcpyAsync(fault, dfault, sizeof(fault), cudaMemcpyDeviceToHost, st));
     if (!on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
     NBX_CUDA(cudaStreamSynchronize(st));
     NBX_CUDA(cudaEventElapsedTime(&plan->last_ms, ctx->ev0, ctx->ev1));
-    ctx->fault_stage = fault[0] != ~0ull ? 0 : 1;
-    if (fault[0] != ~0ull) return (int64_t)fault[0];
-    return fault[1] == ~0ull ? -1 : (int64_t)fault[1];
+    return pick_fault(ctx, fault);
+}
+
+// zlib's CRC-32 (reflected 0xEDB88320), slicing-by-8.
+struct Crc32Tables {
+    uint32_t t[8][256];
+    Crc32Tables() {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            t[0][i] = c;
+        }
+        for (uint32_t i = 0; i < 256; ++i)
+            for (int s = 1; s < 8; ++s) t[s][i] = (t[s - 1][i] >> 8) ^ t[0][t[s - 1][i] & 0xFF];
+    }
+};
+
+uint32_t crc32_update(uint32_t crc, const unsigned char* p, size_t n) {
+    static const Crc32Tables T;
+    uint32_t c = ~crc;
+    while (n >= 8) {
+        uint32_t lo, hi;
+        std::memcpy(&lo, p, 4);
+        std::memcpy(&hi, p + 4, 4);
+        lo ^= c;
+        c = T.t[7][lo & 0xFF] ^ T.t[6][(lo >> 8) & 0xFF] ^ T.t[5][(lo >> 16) & 0xFF] ^ T.t[4][lo >> 24] ^
+            T.t[3][hi & 0xFF] ^ T.t[2][(hi >> 8) & 0xFF] ^ T.t[1][(hi >> 16) & 0xFF] ^ T.t[0][hi >> 24];
+        p += 8;
+        n -= 8;
+    }
+    while (n--) c = T.t[0][(c ^ *p++) & 0xFF] ^ (c >> 8);
+    return ~c;
 }
 
 thread_local std::string g_noctx_err;
@@ -634,6 +694,13 @@ void nbx_ctx_destroy(void* ctxp) {
     cudaStreamSynchronize(ctx->stream);
     delete ctx->oneshot;
     ctx->oneshot = nullptr;
+    for (int b = 0; b < 2; ++b) {
+        delete ctx->camp_plan[b];
+        ctx->camp_out[b].release();
+        ctx->camp_fault[b].release();
+        if (ctx->camp_host[b]) cudaFreeHost(ctx->camp_host[b]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     ctx->out_scratch.release();
     ctx->fault.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -741,6 +808,154 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
     return fault_status(ctxp, bad, first_bad);
 }
 
+// Device copy of a host input (or the device pointer itself).
+const void* stage_input(Ctx* ctx, DevBuf& tmp, const void* data, size_t bytes, int on_device, cudaStream_t s) {
+    if (on_device) return data;
+    tmp.ensure(bytes);
+    NBX_CUDA(cudaMemcpyAsync(tmp.p, data, bytes, cudaMemcpyHostToDevice, s));
+    (void)ctx;
+    return tmp.p;
+}
+
+int nbx_image_stats(void* ctxp, const void* data, int64_t n, int dtype, int on_device, double* out4) {
+    return guarded(ctxp, [&] {
+        if (!ctxp || !out4 || !data) throw ArgError("invalid image_stats arguments");
+        if (n < 1) throw ArgError("image_stats requires a non-empty buffer");
+        if (dtype != 0 && dtype != 1) throw ArgError("dtype must be 0 (f32) or 1 (f64)");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        DevBuf in, parts, res;
+        const void* d = stage_input(ctx, in, data, (size_t)n * (dtype ? 8 : 4), on_device, s);
+        parts.ensure(nbx::stats_scratch_bytes(n));
+        res.ensure(3 * sizeof(double));
+        NBX_CUDA(nbx::launch_stats(d, n, dtype, parts.p, static_cast<double*>(res.p), s));
+        double h[3];
+        NBX_CUDA(cudaMemcpyAsync(h, res.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        out4[0] = h[0];
+        out4[1] = h[1];
+        out4[2] = h[2] / (double)n;
+        out4[3] = h[2];
+        return NBX_OK;
+    });
+}
+
+int nbx_image_histogram(void* ctxp, const void* data, int64_t n, int dtype, int on_device, int n_bins, double lo,
+                        double hi, int64_t* counts, int64_t* underflow, int64_t* overflow) {
+    return guarded(ctxp, [&] {
+        if (!ctxp || !data || !counts) throw ArgError("invalid image_histogram arguments");
+        if (!(lo < hi)) throw ArgError("histogram range must satisfy lo < hi");
+        if (n_bins < 1) throw ArgError("n_bins must be >= 1");
+        if (n < 1) throw ArgError("image_histogram requires a non-empty buffer");
+        if (dtype != 0 && dtype != 1) throw ArgError("dtype must be 0 (f32) or 1 (f64)");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        DevBuf in, cnt;
+        const void* d = stage_input(ctx, in, data, (size_t)n * (dtype ? 8 : 4), on_device, s);
+        cnt.ensure(sizeof(unsigned long long) * ((size_t)n_bins + 2));
+        NBX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * ((size_t)n_bins + 2), s));
+        NBX_CUDA(nbx::launch_histogram(d, n, dtype, n_bins, lo, hi, static_cast<unsigned long long*>(cnt.p), s));
+        std::vector<unsigned long long> h((size_t)n_bins + 2);
+        NBX_CUDA(cudaMemcpyAsync(h.data(), cnt.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < n_bins; ++b) counts[b] = (int64_t)h[b + 1];
+        if (underflow) *underflow = (int64_t)h[0];
+        if (overflow) *overflow = (int64_t)h[(size_t)n_bins + 1];
+        return NBX_OK;
+    });
+}
+
+uint32_t nbx_crc32(uint32_t crc, const void* data, int64_t n) {
+    if (!data || n <= 0) return crc;
+    return crc32_update(crc, static_cast<const unsigned char*>(data), (size_t)n);
+}
+
+int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int compute, const char* const* paths,
+                 uint32_t* crcs, int64_t* first_bad) {
+    if (first_bad) *first_bad = -1;
+    int64_t bad_code = -1;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        if (n_images < 0 || (n_images > 0 && (!descs || !paths || !crcs))) throw ArgError("invalid campaign arguments");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        if (!ctx->copy_stream) NBX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = ctx->stream, ds = ctx->copy_stream;
+        cudaEvent_t kdone[2], copied[2];
+        for (int b = 0; b < 2; ++b) {
+            NBX_CUDA(cudaEventCreateWithFlags(&kdone[b], cudaEventDisableTiming));
+            NBX_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+            if (!ctx->camp_plan[b]) ctx->camp_plan[b] = new Plan();
+            ctx->camp_fault[b].ensure(kFaultSlots * sizeof(unsigned long long));
+        }
+        struct Events {
+            cudaEvent_t* e;
+            ~Events() {
+                for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+            }
+        };
+        cudaEvent_t all[4] = {kdone[0], kdone[1], copied[0], copied[1]};
+        Events guard{all};
+        unsigned long long hfault[2][kFaultSlots];
+        size_t bytes[2] = {0, 0};
+        // render image i into slot i % 2: plan build (host), launch, then async D2H + fault read
+        auto launch = [&](int i) {
+            const int b = i & 1;
+            Plan* plan = build_plan(ctx, descs + i, compute, ctx->camp_plan[b]);
+            bytes[b] = (size_t)plan->n_pixels * 4;
+            ctx->camp_out[b].ensure(bytes[b]);
+            enqueue_plan(plan, NBX_OUT_IMAGE_F32, ctx->camp_out[b].p,
+                         static_cast<unsigned long long*>(ctx->camp_fault[b].p), cs);
+            NBX_CUDA(cudaEventRecord(kdone[b], cs));
+            NBX_CUDA(cudaStreamWaitEvent(ds, kdone[b], 0));
+            NBX_CUDA(cudaMemcpyAsync(hfault[b], ctx->camp_fault[b].p, sizeof(hfault[b]), cudaMemcpyDeviceToHost, ds));
+            NBX_CUDA(cudaMemcpyAsync(ctx->camp_host[b], ctx->camp_out[b].p, bytes[b], cudaMemcpyDeviceToHost, ds));
+            NBX_CUDA(cudaEventRecord(copied[b], ds));
+        };
+        // pinned staging sized once for the largest image (never reallocated mid-pipeline)
+        size_t max_bytes = 0;
+        for (int i = 0; i < n_images; ++i) max_bytes = std::max(max_bytes, (size_t)count_pixels(descs + i) * 4);
+        if (ctx->camp_host_bytes < max_bytes) {
+            for (int q = 0; q < 2; ++q) {
+                if (ctx->camp_host[q]) cudaFreeHost(ctx->camp_host[q]);
+                ctx->camp_host[q] = nullptr;
+            }
+            ctx->camp_host_bytes = 0;
+            for (int q = 0; q < 2; ++q) NBX_CUDA(cudaMallocHost(&ctx->camp_host[q], max_bytes));
+            ctx->camp_host_bytes = max_bytes;
+        }
+        if (n_images > 0) launch(0);
+        for (int i = 0; i < n_images; ++i) {
+            const int b = i & 1;
+            if (i + 1 < n_images) launch(i + 1);  // overlaps the write-out of image i below
+            NBX_CUDA(cudaEventSynchronize(copied[b]));
+            const int64_t bad = pick_fault(ctx, hfault[b]);
+            if (bad >= 0) {
+                bad_code = ((int64_t)i << 40) | bad;
+                NBX_CUDA(cudaStreamSynchronize(cs));
+                NBX_CUDA(cudaStreamSynchronize(ds));
+                return NBX_OK;
+            }
+            crcs[i] = crc32_update(0, static_cast<const unsigned char*>(ctx->camp_host[b]), bytes[b]);
+            FILE* fh = std::fopen(paths[i], "wb");
+            if (!fh) throw ArgError(std::string("cannot open ") + paths[i]);
+            const size_t wrote = std::fwrite(ctx->camp_host[b], 1, bytes[b], fh);
+            const int closed = std::fclose(fh);
+            if (wrote != bytes[b] || closed != 0) throw ArgError(std::string("short write to ") + paths[i]);
+        }
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    if (bad_code >= 0) {
+        if (first_bad) *first_bad = bad_code;
+        set_err(ctxp, "non-finite value in campaign image " + std::to_string(bad_code >> 40));
+        return NBX_ERR_NUMERICAL;
+    }
+    return NBX_OK;
+}
+
 int nbx_fault_stage(void* ctxp) { return ctxp ? static_cast<Ctx*>(ctxp)->fault_stage : 0; }
 
 int nbx_background(void* ctxp, const nbx_spots_desc* d, int out_mode, void* out, int out_on_device,
@@ -787,8 +1002,8 @@ int nbx_background(void* ctxp, const nbx_spots_desc* d, int out_mode, void* out,
             dout = ctx->out_scratch.p;
             if (out_mode == NBX_OUT_ADD_F64) NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, s));
         }
-        ctx->fault.ensure(2 * sizeof(unsigned long long));
-        NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 2 * sizeof(unsigned long long), s));
+        ctx->fault.ensure(kFaultSlots * sizeof(unsigned long long));
+        NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, kFaultSlots * sizeof(unsigned long long), s));
         P.out_mode = out_mode;
         P.out = dout;
         P.fault = static_cast<unsigned long long*>(ctx->fault.p);

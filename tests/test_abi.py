@@ -98,3 +98,11 @@ def test_host_poisson_twin_matches_oracle_build(lib):
     out = np.empty_like(mean)
     assert lib.nbx_poisson_host(mean.ctypes.data, out.ctypes.data, mean.size, 1, 77, 3) == 0
     assert np.array_equal(out, oracle.poisson(mean, 77, 3))
+
+
+def test_crc32_matches_zlib(lib):
+    import zlib
+
+    for n in (0, 1, 7, 8, 9, 4096, 100003):
+        b = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
+        assert lib.nbx_crc32(0, b.ctypes.data, n) == zlib.crc32(b.tobytes())

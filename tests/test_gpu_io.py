@@ -1,0 +1,65 @@
+"""GPU: pipelined campaign (F3) against the staged path + reference file format, and device stats (F4)."""
+import json
+import zlib
+
+import numpy as np
+import pytest
+
+from paper_2205_07976_b200 import BackgroundProfile, PixelBuffer, simulate_image, synthetic
+from paper_2205_07976_b200 import io as nio
+
+pytestmark = pytest.mark.gpu
+
+WATER = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.162, 8.0), (0.3, 6.5)))
+
+
+def ctx_for(i, compute="fp32"):
+    panel = synthetic.roi(synthetic.rayonix_panel(), 1700, 1800, 96, 128)
+    return synthetic.ls49_context(synthetic.SEED + i, panel=panel, n_channels=10, n_domains=4, compute=compute)
+
+
+@pytest.mark.parametrize("compute", ["fp32", "fp64"])
+def test_campaign_files_equal_simulate_image_downcast(gpu, tmp_path, compute):
+    res = nio.run_campaign(lambda i: ctx_for(i, compute), 5, tmp_path, first_image=10, background=WATER,
+                           thickness_factor=0.5, seeds=lambda i: synthetic.SEED + i)
+    assert res.indices == list(range(10, 15))
+    for idx, path, crc in zip(res.indices, res.paths, res.crcs):
+        data, side = nio.read_image(path)
+        assert side["crc32"] == crc == zlib.crc32(path.read_bytes())
+        assert side["image_index"] == idx and side["seed"] == synthetic.SEED + idx
+        assert side["dims"] == [96, 128] and side["dtype"] == "float32"
+        acc = simulate_image(ctx_for(idx, compute), background=WATER, thickness_factor=0.5)
+        assert np.array_equal(data.reshape(-1), acc.data.astype(np.float32))
+
+
+def test_write_image_matches_reference_format(gpu, tmp_path):
+    acc = simulate_image(ctx_for(0))
+    p = nio.write_image(acc, tmp_path / "x", panel=ctx_for(0).panel, spectrum=ctx_for(0).spectrum, seed=3,
+                        image_index=7)
+    side = json.loads((tmp_path / "x.json").read_text())
+    assert set(side) == {"dims", "dtype", "byte_order", "downcast", "pixel_size_m", "distance_m",
+                         "wavelengths_angstrom", "seed", "image_index", "crc32"}
+    data, _ = nio.read_image(p)
+    assert np.array_equal(data.reshape(-1), acc.data.astype("<f4"))
+
+
+def test_image_stats_and_histogram(gpu):
+    rng = np.random.default_rng(17)
+    vals = rng.uniform(-1, 1, 1_000_000)
+    st = nio.image_stats(PixelBuffer((1000, 1000), "f64", vals))
+    assert st.min == vals.min() and st.max == vals.max()
+    assert st.total == pytest.approx(float(np.sum(vals)), rel=1e-12)
+    assert nio.image_stats(PixelBuffer((2, 2), "f64", [1.0, 2.0, 3.0, 4.0])) == (1.0, 4.0, 2.5, 10.0)
+    c = nio.image_stats(PixelBuffer((3, 5), "f32", np.full(15, 7.25)))
+    assert c.min == c.max == c.mean == 7.25 and c.total == 7.25 * 15
+    # determinism: same bits every call
+    assert nio.image_stats(PixelBuffer((1000, 1000), "f64", vals)) == st
+    vals = rng.uniform(-0.2, 1.2, 100_000)
+    h = nio.image_histogram(PixelBuffer((250, 400), "f64", vals), 64, (0.0, 1.0))
+    under, over = int((vals < 0).sum()), int((vals > 1).sum())
+    idx = np.clip(np.floor((vals[(vals >= 0) & (vals <= 1)] - 0.0) / (1.0 / 64)).astype(np.int64), 0, 63)
+    assert h.counts.tolist() == np.bincount(idx, minlength=64).tolist()
+    assert (h.underflow, h.overflow) == (under, over)
+    assert h.cumulative.tolist() == np.cumsum(h.counts).tolist()
+    edge = nio.image_histogram(PixelBuffer((1, 4), "f64", [1.0] * 4), 4, (0.0, 1.0))
+    assert edge.counts.tolist() == [0, 0, 0, 4]
