@@ -198,9 +198,6 @@ __device__ __forceinline__ T shape_latt2(T hrad2, T nnn) {
 
 }  // namespace nbx
 
-#ifndef NBX_K_FRND
-#define NBX_K_FRND 0
-#endif
 
 namespace nbx {
 
@@ -245,6 +242,16 @@ __device__ __forceinline__ f2x add2(f2x a, f2x b) {
     return d;
 }
 
+#ifndef NBX_NUM_MUFU
+#define NBX_NUM_MUFU 1  // 0: polynomial numerator on every FP32 variant (the pre-MUFU kernel)
+#endif
+constexpr float kSinLinear = 0.0099f;
+__device__ __forceinline__ float sin_approx_f32(float x) {
+    float y;
+    asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <int DEG>
 __device__ __forceinline__ f2x q_sinpi_f32x2(f2x s) {
     if constexpr (DEG == 3) {
@@ -263,9 +270,22 @@ struct AxisF32x2 {
     f2x num, den, j, m;
 };
 
+// Numerator of the degree-3 (default) packed path: sin(pi N t) on the XU pipe
+// (MUFU.SIN), taking 6 of the 8 FMA-pipe ops of the polynomial form off the
+// FMA pipe, which bounds this loop.  MUFU.SIN's absolute error is ~3.4e-7 on
+// [-pi, pi] and <= 1.3e-6 up to 10 rad (tools/probes/mix_probe.cu), harmless
+// where the numerator is large; near zero its output is fixed-point (~1.6e-7
+// absolute), so below |x| = kSinLinear the argument itself is used (relative
+// error <= x^2/6 = 1.6e-5; the compiler predicates the MUFU, no select).  The
+// numerator is then pi x the polynomial form's (which carries sin(pi r)/pi), so
+// a chunk sum is pi^6 times the reference's; domain_sum_f32 rescales it.
+template <int DEG>
+constexpr bool kMufuNum = (DEG == 3) && (NBX_NUM_MUFU != 0);
+
 // Unbiased (hot-loop) axis for two channels: the same arithmetic as axis_f32
 // without |t| (signs drop out of the squared ratio) and without the bias
-// (t == 0 -> 0/0 is caught by the caller's finiteness check).
+// (t == 0 -> 0/0 is caught by the caller's finiteness check).  With the MUFU
+// numerator N must be passed as pi N.
 template <int DEG>
 __device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x magic) {
     AxisF32x2 a;
@@ -274,15 +294,17 @@ __device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x
     a.m = add2(x, magic);
     a.j = fma2(magic, neg1, a.m);         // m - magic = rint(x), exact
     const f2x t = fma2(a.j, neg1, x);     // x - j, exact
-#if NBX_K_FRND
-    // k = rint(N t) on the XU pipe (FRND), which the FP32 loop leaves mostly idle
-    const f2x u = mul2(N, t);
-    const f2x r = fma2(N, t, pk2(-rintf(lo2(u)), -rintf(hi2(u))));  // N t - k, one rounding
-#else
-    const f2x nk = fma2(fma2(N, t, M), neg1, M);  // -rint(N t)
-    const f2x r = fma2(N, t, nk);         // N t - rint(N t)
-#endif
-    a.num = mul2(r, q_sinpi_f32x2<DEG>(mul2(r, r)));
+    if constexpr (kMufuNum<DEG>) {
+        const f2x arg = mul2(N, t);           // pi N t (radians)
+        const float a0 = lo2(arg), a1 = hi2(arg);
+        const float s0 = fabsf(a0) < kSinLinear ? a0 : sin_approx_f32(a0);
+        const float s1 = fabsf(a1) < kSinLinear ? a1 : sin_approx_f32(a1);
+        a.num = pk2(s0, s1);
+    } else {
+        const f2x nk = fma2(fma2(N, t, M), neg1, M);  // -rint(N t)
+        const f2x r = fma2(N, t, nk);                 // N t - rint(N t)
+        a.num = mul2(r, q_sinpi_f32x2<DEG>(mul2(r, r)));
+    }
     a.den = mul2(t, q_sinpi_f32x2<DEG>(mul2(t, t)));
     return a;
 }

@@ -65,7 +65,7 @@ __device__ __forceinline__ double background_value(const SpotsParams& P, const D
 }
 
 #ifndef NBX_MIN_BLOCKS_F32
-#define NBX_MIN_BLOCKS_F32 2  // 128 registers for the 4x-unrolled packed loop
+#define NBX_MIN_BLOCKS_F32 3  // 80 registers: the MUFU-numerator loop gains from 24 warps/SM
 #endif
 #ifndef NBX_PAIR_UNROLL
 #define NBX_PAIR_UNROLL 4  // measured best with 2 blocks / 128 registers (more ILP beats occupancy)
@@ -83,6 +83,7 @@ constexpr int kBlockY = 8;
 constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
 constexpr int kPolyF64 = 6;  // FP64 Q(s) degree (rel err 1.2e-13)
 constexpr int kNewtonF64 = 1;
+constexpr double kInvPi6 = 1.0 / 961.38919357530443703021944;  // pi^-6
 
 // ---------------------------------------------------------------------------
 // Sum over channels of w * F^2 * F_latt^2 for one (pixel, sub-pixel, domain).
@@ -145,9 +146,9 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
                                                  float magic_c, const float* __restrict__ base) {
     const f2x Sa = bc2(a_hi), Sb = bc2(b_hi), Sc = bc2(c_hi);
     const f2x Fa = bc2(fa), Fb = bc2(fb), Fc = bc2(fc);
-    const f2x Na = bc2(P.n_cells_f[0]), Nb = bc2(P.n_cells_f[1]), Nc = bc2(P.n_cells_f[2]);
+    const float nf = kMufuNum<PDEG> ? 3.14159265358979323846f : 1.0f;  // MUFU numerator takes pi N
+    const f2x Na = bc2(nf * P.n_cells_f[0]), Nb = bc2(nf * P.n_cells_f[1]), Nc = bc2(nf * P.n_cells_f[2]);
     const f2x M = bc2(kMagicF32), Mc = bc2(magic_c);
-    const f2x sH = bc2((float)P.sH), sK = bc2((float)P.sK);
     f2x acc = bc2(0.0f);
 #pragma unroll kPairUnroll
     for (int q = p0; q < p1; ++q) {
@@ -196,6 +197,15 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         } else {
             accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, false>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa,
                                                                   fb, fc, magic_c, base);
+        }
+        if constexpr (SHAPE == 0 && !WIDE && kMufuNum<PDEG>) {
+            // MUFU numerators are sin(pi N t), the polynomial denominators sin(pi t)/pi
+            if (isfinite(accf))
+                dacc += (double)accf * kInvPi6;
+            else  // exact Bragg position / underflow: the reference's limit branch (polynomial form)
+                dacc += (double)chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi,
+                                                                              c_hi, fa, fb, fc, magic_c, base);
+            continue;
         }
         if constexpr (SHAPE == 0) {
             if (!isfinite(accf))  // exact Bragg position / underflow: the reference's limit branch

@@ -438,9 +438,13 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             std::vector<nbx::ChunkF32> chunks;
             std::vector<float> ch;
             int i0 = 0, npairs = 0;
+            const char* cev = std::getenv("NBX_CHUNK_MAX");
+            const int chunk_max = cev ? std::max(2, std::atoi(cev)) : 64;
+            const char* pev = std::getenv("NBX_PAD_PAIRS");
+            const int pad_pairs = pev ? std::max(1, std::atoi(pev)) : 1;
             while (i0 < n_src) {
                 int i1 = i0 + 1;
-                while (i1 < n_src && i1 - i0 < 64 && (iv[order[i1]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++i1;
+                while (i1 < n_src && i1 - i0 < chunk_max && (iv[order[i1]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++i1;
                 const double iv0 = 0.5 * (iv[order[i0]] + iv[order[i1 - 1]]);
                 const int p0 = npairs;
                 for (int q = i0; q < i1; q += 2) {
@@ -449,6 +453,12 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                     ch.push_back((float)(iv[order[q1]] - iv0));
                     ch.push_back((float)d->weights[sb + order[q]]);
                     ch.push_back(q + 1 < i1 ? (float)d->weights[sb + order[q1]] : 0.0f);
+                    ++npairs;
+                }
+                while ((npairs - p0) % pad_pairs) {  // zero-weight pairs up to a multiple of the unroll
+                    for (int r = 0; r < 2; ++r) ch.push_back((float)(iv[order[i1 - 1]] - iv0));
+                    ch.push_back(0.0f);
+                    ch.push_back(0.0f);
                     ++npairs;
                 }
                 chunks.push_back(nbx::ChunkF32{iv0, p0, npairs});
