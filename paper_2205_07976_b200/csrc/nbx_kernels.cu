@@ -100,13 +100,24 @@ constexpr double kInvPi6 = 1.0 / 961.38919357530443703021944;  // pi^-6
 // by the index FMA chain is directly the biased cell number.
 // ---------------------------------------------------------------------------
 
+// The few launch constants the scalar form needs, passed BY VALUE: a reference
+// to the kernel's parameter block would make the compiler copy all of it into
+// a local-memory stack frame in every thread (256 B of stores per pixel).
+struct ScalarArgs {
+    float Na, Nb, Nc, nnn;
+    int32_t sH, sK, sh_h, sh_k;
+};
+
+__device__ __forceinline__ ScalarArgs scalar_args(const SpotsParams& P) {
+    return ScalarArgs{P.n_cells_f[0], P.n_cells_f[1], P.n_cells_f[2], P.nnn_f, P.sH, P.sK, P.sh_h, P.sh_k};
+}
+
 // Scalar form: the biased re-evaluation, the non-grating shapes, the WIDE index.
 template <int SHAPE, bool WIDE, int PDEG, bool BIAS>
-__device__ __noinline__ float chunk_sum_f32_scalar(const SpotsParams& P, const float4* __restrict__ sch, int p0,
+__device__ __noinline__ float chunk_sum_f32_scalar(const ScalarArgs P, const float4* __restrict__ sch, int p0,
                                                    int p1, float a_hi, float b_hi, float c_hi, float fa, float fb,
                                                    float fc, float magic_c, const float* __restrict__ base) {
-    const float Na = P.n_cells_f[0], Nb = P.n_cells_f[1], Nc = P.n_cells_f[2];
-    const float sHf = (float)P.sH, sKf = (float)P.sK;
+    const float Na = P.Na, Nb = P.Nb, Nc = P.Nc;
     float accf = 0.0f;
     for (int q = 2 * p0; q < 2 * p1; ++q) {
         const float4 c4 = sch[q >> 1];
@@ -122,7 +133,7 @@ __device__ __noinline__ float chunk_sum_f32_scalar(const SpotsParams& P, const f
             L2 = ratio * ratio;
         } else {
             const float x = Na * A.t, y = Nb * B.t, z = Nc * C.t;
-            L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn_f);
+            L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn);
         }
         float F2;
         if constexpr (!WIDE) {
@@ -195,7 +206,7 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         if constexpr (SHAPE == 0 && !WIDE) {
             accf = chunk_sum_f32x2<PDEG>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb, fc, magic_c, base);
         } else {
-            accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, false>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa,
+            accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, false>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa,
                                                                   fb, fc, magic_c, base);
         }
         if constexpr (SHAPE == 0 && !WIDE && kMufuNum<PDEG>) {
@@ -203,13 +214,13 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
             if (isfinite(accf))
                 dacc += (double)accf * kInvPi6;
             else  // exact Bragg position / underflow: the reference's limit branch (polynomial form)
-                dacc += (double)chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi,
+                dacc += (double)chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi,
                                                                               c_hi, fa, fb, fc, magic_c, base);
             continue;
         }
         if constexpr (SHAPE == 0) {
             if (!isfinite(accf))  // exact Bragg position / underflow: the reference's limit branch
-                accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi,
+                accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi, c_hi,
                                                                      fa, fb, fc, magic_c, base);
         }
         dacc += (double)accf;
@@ -280,8 +291,8 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
 
     const DevPanel& pan = P.panels[blockIdx.z];
     const int f = blockIdx.x * kBlockX + threadIdx.x;
-    const int sl = blockIdx.y * kBlockY + threadIdx.y;
-    if (sl >= pan.slow || f >= pan.fast) return;
+    const int sl = P.row0 + blockIdx.y * kBlockY + threadIdx.y;
+    if (sl >= pan.slow || sl >= P.max_slow || f >= pan.fast) return;
 
     const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
     const double ps = pan.pixel_size;
@@ -393,8 +404,8 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
 __global__ void __launch_bounds__(kBlockX* kBlockY) background_kernel(const SpotsParams P) {
     const DevPanel& pan = P.panels[blockIdx.z];
     const int f = blockIdx.x * kBlockX + threadIdx.x;
-    const int sl = blockIdx.y * kBlockY + threadIdx.y;
-    if (sl >= pan.slow || f >= pan.fast) return;
+    const int sl = P.row0 + blockIdx.y * kBlockY + threadIdx.y;
+    if (sl >= pan.slow || sl >= P.max_slow || f >= pan.fast) return;
     const int64_t p = pan.out_offset + (int64_t)sl * pan.fast + f;
     const double v = background_value(P, pan, sl, f);
     bool bad;
@@ -454,7 +465,7 @@ static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) 
         if (e != cudaSuccess) return e;
     }
     dim3 block(kBlockX, kBlockY, 1);
-    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow + kBlockY - 1) / kBlockY, P.n_panels);
+    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow - P.row0 + kBlockY - 1) / kBlockY, P.n_panels);
     k<<<grid, block, smem, st>>>(P);
     return cudaGetLastError();
 }
@@ -490,7 +501,7 @@ static int grid_for(int64_t n, int block) {
 
 cudaError_t launch_background(const SpotsParams& P, cudaStream_t st) {
     dim3 block(kBlockX, kBlockY, 1);
-    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow + kBlockY - 1) / kBlockY, P.n_panels);
+    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow - P.row0 + kBlockY - 1) / kBlockY, P.n_panels);
     background_kernel<<<grid, block, 0, st>>>(P);
     return cudaGetLastError();
 }

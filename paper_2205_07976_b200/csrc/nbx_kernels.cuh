@@ -60,7 +60,8 @@ struct SpotsParams {
     double out_scale;              // r_e^2 fluence / norm (/ sigma on the FP32 path)
     void* out;
     unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none
-    int32_t max_slow, max_fast;
+    int32_t max_slow, max_fast;    // launch covers rows [row0, max_slow) of every panel
+    int32_t row0, pad2;            // first row of this launch (row bands of a pipelined run)
     // diffuse background (kernels.py:279-312)
     const double2* bg_chan;        // {lambda, w} of every source
     const double* bg_stol;

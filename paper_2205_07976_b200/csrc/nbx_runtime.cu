@@ -54,6 +54,30 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 // Device buffer that frees itself.
+// Pinned host staging buffer (grown, never shrunk) for table uploads.
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { release(); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* ensure(size_t n) {
+        if (n * sizeof(T) > bytes) {
+            release();
+            NBX_CUDA(cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocDefault));
+            bytes = n * sizeof(T);
+        }
+        return static_cast<T*>(p);
+    }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -89,6 +113,11 @@ struct Ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // pipelined host-output runs: a second compute stream (row bands alternate so
+    // one band's tail overlaps the next band's head) and one event per band
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t band_ev[16] = {};
+    cudaEvent_t join_ev = nullptr;
     DevBuf out_scratch;     // device image when the caller passes host memory
     DevBuf fault;           // one u64
     std::string err;
@@ -107,7 +136,9 @@ struct Plan {
     bool wide = false;
     nbx::SpotsParams P{};
     DevBuf panels, bases, chan, chunks, table;
+    HostBuf host_table;       // pinned staging of the F^2 grid
     BgBufs bg;
+    bool uniform_panels = true;  // every panel has the same (slow, fast): row bands are 2-D copies
     int64_t n_pixels = 0;
     int64_t steps = 0;
     nbx_plan_info_t info{};
@@ -344,6 +375,8 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         const std::vector<nbx::DevPanel> hp = make_panels(d, &max_slow, &max_fast, &off, &sub_steps);
         plan->n_pixels = off;
         plan->steps = sub_steps * (int64_t)n_src * d->n_domains;
+        plan->uniform_panels = true;
+        for (const auto& q : hp) plan->uniform_panels &= (q.slow == max_slow && q.fast == max_fast);
 
         // reachable Miller box (+1 margin for rounding) -> dense grid
         const double relmax = max_rel(d);
@@ -395,18 +428,20 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         for (int dd = 0; dd < d->n_domains; ++dd)
             for (int a = 0; a < 3; ++a) smax = std::max(smax, norm3(d->bases + 9 * dd + 3 * a) * relmax);
 
-        // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma)
+        // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma), built straight
+        // into pinned staging memory: first the largest reachable F^2, then the fill
         const double def2 = d->default_f * d->default_f;
-        std::vector<double> f2(cells_alloc, def2);
+        auto reachable = [&](int i) {
+            return std::abs(d->hkl[3 * i]) <= hmax[0] && std::abs(d->hkl[3 * i + 1]) <= hmax[1] &&
+                   std::abs(d->hkl[3 * i + 2]) <= hmax[2];
+        };
+        auto cell_of = [&](int i) {
+            return (int64_t)(d->hkl[3 * i] + hmax[0]) * P.sH + (int64_t)(d->hkl[3 * i + 1] + hmax[1]) * P.sK +
+                   (d->hkl[3 * i + 2] + hmax[2]);
+        };
         double maxf2 = def2;
-        for (int i = 0; i < d->n_entries; ++i) {
-            const int h = d->hkl[3 * i], k = d->hkl[3 * i + 1], l = d->hkl[3 * i + 2];
-            if (std::abs(h) > hmax[0] || std::abs(k) > hmax[1] || std::abs(l) > hmax[2]) continue;  // unreachable
-            const double F = d->amplitudes[i];
-            const int64_t idx = (int64_t)(h + hmax[0]) * P.sH + (int64_t)(k + hmax[1]) * P.sK + (l + hmax[2]);
-            f2[idx] = F * F;
-            maxf2 = std::max(maxf2, F * F);
-        }
+        for (int i = 0; i < d->n_entries; ++i)
+            if (reachable(i)) maxf2 = std::max(maxf2, d->amplitudes[i] * d->amplitudes[i]);
         double sigma = 1.0;
         if (compute == NBX_COMPUTE_FP32) {
             double maxw = 0.0;
@@ -418,6 +453,15 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 e = std::max(-1000, std::min(e, 100));
                 sigma = std::ldexp(1.0, e);
             }
+            float* tf = plan->host_table.ensure<float>(cells_alloc);
+            std::fill(tf, tf + cells_alloc, (float)(def2 * sigma));
+            for (int i = 0; i < d->n_entries; ++i)
+                if (reachable(i)) tf[cell_of(i)] = (float)(d->amplitudes[i] * d->amplitudes[i] * sigma);
+        } else {
+            double* t64 = plan->host_table.ensure<double>(cells_alloc);
+            std::fill(t64, t64 + cells_alloc, def2);
+            for (int i = 0; i < d->n_entries; ++i)
+                if (reachable(i)) t64[cell_of(i)] = d->amplitudes[i] * d->amplitudes[i];
         }
         plan->out_scale = plan->scale / sigma;
 
@@ -472,10 +516,9 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                                 cudaMemcpyHostToDevice));
             P.chunks = static_cast<const nbx::ChunkF32*>(plan->chunks.p);
             P.n_chunks = (int32_t)chunks.size();
-            std::vector<float> tf(cells_alloc);
-            for (int64_t i = 0; i < cells_alloc; ++i) tf[i] = (float)(f2[i] * sigma);
             plan->table.ensure(cells_alloc * sizeof(float));
-            NBX_CUDA(cudaMemcpy(plan->table.p, tf.data(), cells_alloc * sizeof(float), cudaMemcpyHostToDevice));
+            NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells_alloc * sizeof(float),
+                                cudaMemcpyHostToDevice));
         } else {
             std::vector<double> ch(2 * (size_t)n_src);
             for (int i = 0; i < n_src; ++i) {
@@ -485,7 +528,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             plan->chan.ensure(ch.size() * sizeof(double));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice));
             plan->table.ensure(cells * sizeof(double));
-            NBX_CUDA(cudaMemcpy(plan->table.p, f2.data(), cells * sizeof(double), cudaMemcpyHostToDevice));
+            NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells * sizeof(double), cudaMemcpyHostToDevice));
         }
         if ((size_t)n_src * 16 > 200 * 1024) throw ArgError("too many sources in one shard (max 12800)");
 
@@ -555,25 +598,59 @@ int64_t pick_fault(Ctx* ctx, const unsigned long long* fault) {
     return -1;
 }
 
-// Enqueue one spot launch of `plan` into device buffer `dout` with fault slots `fault`.
-void enqueue_plan(Plan* plan, int mode, void* dout, unsigned long long* fault, cudaStream_t st) {
-    NBX_CUDA(cudaMemsetAsync(fault, 0xFF, kFaultSlots * sizeof(unsigned long long), st));
+// Launch the spot kernel of `plan` over rows [row0, row1) of every panel.
+void launch_rows(Plan* plan, int mode, void* dout, unsigned long long* fault, cudaStream_t st, int row0, int row1) {
     nbx::SpotsParams P = plan->P;
     P.out_mode = mode;
     P.out = dout;
     P.fault = fault;
     P.fault_bg = fault + 1;  // fault_bg[1] = the downcast slot
+    P.row0 = row0;
+    P.max_slow = row1;
     NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
 }
 
+// Enqueue one spot launch of `plan` into device buffer `dout` with fault slots `fault`.
+void enqueue_plan(Plan* plan, int mode, void* dout, unsigned long long* fault, cudaStream_t st) {
+    NBX_CUDA(cudaMemsetAsync(fault, 0xFF, kFaultSlots * sizeof(unsigned long long), st));
+    launch_rows(plan, mode, dout, fault, st, 0, plan->P.max_slow);
+}
+
+// Row bands of a pipelined host-output run (0: one launch, copy afterwards).
+constexpr int kBands = 8;
+int band_rows(const Plan* plan, int mode, int on_device) {
+    const bool write_only = mode == NBX_OUT_F32 || mode == NBX_OUT_F64 || mode == NBX_OUT_IMAGE_F32 ||
+                            mode == NBX_OUT_IMAGE_F64;
+    if (on_device || !write_only || !plan->uniform_panels || plan->n_pixels < (int64_t(1) << 20)) return 0;
+    const char* ev = std::getenv("NBX_BANDS");
+    const int nb = ev ? std::max(1, std::min(16, std::atoi(ev))) : kBands;
+    if (nb <= 1) return 0;
+    const int rows = plan->P.max_slow;
+    return ((rows + nb - 1) / nb + 7) / 8 * 8;  // whole 8-row block lines per band
+}
+
+void ensure_band_resources(Ctx* ctx) {
+    if (!ctx->stream2) NBX_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    if (!ctx->copy_stream) NBX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    if (!ctx->join_ev) NBX_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    for (auto& e : ctx->band_ev)
+        if (!e) NBX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 // Run a plan into `out`; returns the lowest non-finite pixel or -1.
+//
+// With a host `out` the image is computed in row bands that alternate between
+// two compute streams, and band b's download (a 2-D copy: the same rows of every
+// panel) runs on the copy stream while later bands compute, so only the last
+// band's download is exposed (the reference-facing call's end-to-end time).
 int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
     check_mode(mode);
     if (!out) throw ArgError("output buffer is NULL");
     Ctx* ctx = plan->ctx;
     NBX_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
-    const size_t bytes = (size_t)plan->n_pixels * out_elem_bytes(mode);
+    const size_t es = out_elem_bytes(mode);
+    const size_t bytes = (size_t)plan->n_pixels * es;
     void* dout = out;
     if (!on_device) {
         ctx->out_scratch.ensure(bytes);
@@ -583,14 +660,45 @@ int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
     }
     ctx->fault.ensure(kFaultSlots * sizeof(unsigned long long));
     unsigned long long* dfault = static_cast<unsigned long long*>(ctx->fault.p);
-    NBX_CUDA(cudaEventRecord(ctx->ev0, st));
-    enqueue_plan(plan, mode, dout, dfault, st);
-    NBX_CUDA(cudaEventRecord(ctx->ev1, st));
-    plan->timed = true;
     unsigned long long fault[kFaultSlots] = {~0ull, ~0ull, ~0ull};
-    NBX_CUDA(cudaMemcpyAsync(fault, dfault, sizeof(fault), cudaMemcpyDeviceToHost, st));
-    if (!on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
-    NBX_CUDA(cudaStreamSynchronize(st));
+    const int per = band_rows(plan, mode, on_device);
+    if (per == 0) {
+        NBX_CUDA(cudaEventRecord(ctx->ev0, st));
+        enqueue_plan(plan, mode, dout, dfault, st);
+        NBX_CUDA(cudaEventRecord(ctx->ev1, st));
+        NBX_CUDA(cudaMemcpyAsync(fault, dfault, sizeof(fault), cudaMemcpyDeviceToHost, st));
+        if (!on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
+        NBX_CUDA(cudaStreamSynchronize(st));
+    } else {
+        ensure_band_resources(ctx);
+        cudaStream_t s2 = ctx->stream2, cs = ctx->copy_stream;
+        const int rows = plan->P.max_slow, fast = plan->P.max_fast;
+        const size_t pitch = (size_t)rows * fast * es;  // one panel
+        NBX_CUDA(cudaEventRecord(ctx->ev0, st));
+        NBX_CUDA(cudaMemsetAsync(dfault, 0xFF, kFaultSlots * sizeof(unsigned long long), st));
+        NBX_CUDA(cudaEventRecord(ctx->join_ev, st));
+        NBX_CUDA(cudaStreamWaitEvent(s2, ctx->join_ev, 0));
+        int nb = 0;
+        for (int r0 = 0; r0 < rows; r0 += per, ++nb) {  // all launches first: the copies below block the host
+            cudaStream_t s = (nb & 1) ? s2 : st;
+            launch_rows(plan, mode, dout, dfault, s, r0, std::min(rows, r0 + per));
+            NBX_CUDA(cudaEventRecord(ctx->band_ev[nb], s));
+        }
+        NBX_CUDA(cudaEventRecord(ctx->join_ev, s2));
+        NBX_CUDA(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+        NBX_CUDA(cudaEventRecord(ctx->ev1, st));
+        for (int b = 0; b < nb; ++b) {
+            const int r0 = b * per, r1 = std::min(rows, r0 + per);
+            const size_t off = (size_t)r0 * fast * es, width = (size_t)(r1 - r0) * fast * es;
+            NBX_CUDA(cudaStreamWaitEvent(cs, ctx->band_ev[b], 0));
+            NBX_CUDA(cudaMemcpy2DAsync(static_cast<char*>(out) + off, pitch, static_cast<const char*>(dout) + off,
+                                       pitch, width, (size_t)plan->P.n_panels, cudaMemcpyDeviceToHost, cs));
+        }
+        NBX_CUDA(cudaMemcpyAsync(fault, dfault, sizeof(fault), cudaMemcpyDeviceToHost, st));
+        NBX_CUDA(cudaStreamSynchronize(cs));
+        NBX_CUDA(cudaStreamSynchronize(st));
+    }
+    plan->timed = true;
     NBX_CUDA(cudaEventElapsedTime(&plan->last_ms, ctx->ev0, ctx->ev1));
     return pick_fault(ctx, fault);
 }
@@ -711,6 +819,10 @@ void nbx_ctx_destroy(void* ctxp) {
         if (ctx->camp_host[b]) cudaFreeHost(ctx->camp_host[b]);
     }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+    if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+    for (auto e : ctx->band_ev)
+        if (e) cudaEventDestroy(e);
     ctx->out_scratch.release();
     ctx->fault.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -263,6 +263,34 @@ def test_plan_runs_into_device_memory(gpu):
     assert plan.kernel_ms > 0
 
 
+@pytest.mark.parametrize("layout", ["single", "panels"])
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_pipelined_host_download_is_bitwise_the_device_image(gpu, layout, compute):
+    """Host-output runs of >= 2^20 pixels are computed in row bands on two streams with the
+    download of each band overlapping later bands (nbx_runtime.cu:run_plan); every pixel must
+    equal the single-launch device-output image bit for bit, ragged last band included."""
+    import torch
+
+    from paper_2205_07976_b200 import _native as N
+
+    if layout == "single":  # 1030 rows: the last of 8 bands is ragged (1030 = 7 x 136 + 78)
+        panel = synthetic.roi(synthetic.rayonix_panel(), 1400, 1400, 1030, 1024)
+    else:  # 20 uniform panels of 254 x 254 (Jungfrau-like): 2-D band copies across panels
+        panel = synthetic.jungfrau_detector(n_side=5, size=254, thickness=0.0)
+        panel = Detector(panel.panels[:20])
+    ctx = synthetic.ls49_context(panel=panel, n_channels=3, n_domains=2, compute=compute)
+    plan = SpotsPlan(ctx)
+    assert plan.n_pixels >= 1 << 20
+    for mode, dt, tdt in ((N.OUT_F32, np.float32, torch.float32), (N.OUT_F64, np.float64, torch.float64)):
+        dev = torch.zeros(plan.n_pixels, dtype=tdt, device="cuda")
+        torch.cuda.synchronize()
+        plan.run(dev.data_ptr(), mode=mode, on_device=True)
+        host = np.full(plan.n_pixels, np.nan, dtype=dt)
+        plan.run(host, mode=mode)
+        assert np.array_equal(dev.cpu().numpy(), host)
+    plan.close()
+
+
 def test_add_array_upcast_semantics(gpu):
     lhs = PixelBuffer((1, 3), "f64", [0.0, 1.0, 2.0])
     rhs = PixelBuffer((1, 3), "f32", [0.1, 0.5, 0.25])
