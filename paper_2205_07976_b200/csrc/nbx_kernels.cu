@@ -157,8 +157,8 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
                                                  float magic_c, const float* __restrict__ base) {
     const f2x Sa = bc2(a_hi), Sb = bc2(b_hi), Sc = bc2(c_hi);
     const f2x Fa = bc2(fa), Fb = bc2(fb), Fc = bc2(fc);
-    const float nf = kMufuNum<PDEG> ? 3.14159265358979323846f : 1.0f;  // MUFU numerator takes pi N
-    const f2x Na = bc2(nf * P.n_cells_f[0]), Nb = bc2(nf * P.n_cells_f[1]), Nc = bc2(nf * P.n_cells_f[2]);
+    const float* nv = kMufuNum<PDEG> ? P.n_pi_f : P.n_cells_f;  // the MUFU numerator takes pi N
+    const f2x Na = bc2(nv[0]), Nb = bc2(nv[1]), Nc = bc2(nv[2]);
     const f2x M = bc2(kMagicF32), Mc = bc2(magic_c);
     f2x acc = bc2(0.0f);
 #pragma unroll kPairUnroll

@@ -50,6 +50,8 @@ struct SpotsParams {
     int32_t out_mode;              // NBX_OUT_*
     double n_cells_d[3];
     float n_cells_f[3];
+    float n_pi_f[3];               // FP32 MUFU numerator: pi * N (rounded once, on the host)
+    float pad3;
     float nnn_f;                   // Na*Nb*Nc
     double nnn_d;
     // dense-grid index: idx = (n_h - lo_h) * sH + (n_k - lo_k) * sK + (n_l - lo_l)

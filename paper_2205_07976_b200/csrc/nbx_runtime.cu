@@ -549,6 +549,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             P.beam[a] = d->beam_direction[a];
             P.n_cells_d[a] = (double)d->n_cells[a];
             P.n_cells_f[a] = (float)d->n_cells[a];
+            P.n_pi_f[a] = (float)(3.14159265358979323846 * (double)d->n_cells[a]);
         }
         P.nnn_d = (double)d->n_cells[0] * d->n_cells[1] * d->n_cells[2];
         P.nnn_f = (float)P.nnn_d;
