@@ -136,6 +136,9 @@ typedef struct nbx_plan_info_t {
     int32_t compute;             /* NBX_COMPUTE_* */
     int32_t table_kind;          /* 0 dense grid (magic index), 1 dense grid (wide index) */
     double scale;                /* r_e^2 * fluence / norm */
+    int32_t channel_runs;        /* FP64 path: uniform 1/lambda runs evaluated by the channel
+                                    recurrence (0: direct per-channel evaluation) */
+    int32_t reserved;
 } nbx_plan_info_t;
 
 int nbx_version(void);

@@ -270,7 +270,114 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 }
 
 // ---------------------------------------------------------------------------
-// The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path.
+// FP64 path, channel recurrence (sincg, spectra whose 1/lambda form arithmetic
+// progressions -- every BASELINE config: E_j = E_0 + j dE).  Along a run the
+// phase of each axis advances by Delta = S delta per channel, so
+//     z_den = e^{i pi h_w}  and  z_num = e^{i pi N h_w}
+// are complex rotations (2 DMUL + 2 DFMA each) instead of two degree-6
+// polynomials and a range reduction; sin(pi h) and sin(pi N h) are their
+// imaginary parts (signs drop out of F_latt^2).  Anchors and rotation factors
+// come from sincospi once per (pixel, sub-pixel, domain, run).  The rotations
+// drift by ~k ulp after k channels, i.e. an ABSOLUTE error of ~1e-14 in each
+// sine: harmless except where the denominator itself is small, so a channel
+// with any |sin(pi h)| < kRecSmall is evaluated directly from the exact
+// reduced phase t = h - n (axis_f64) -- per-step relative error stays below
+// ~3e-11.  The Fhkl index keeps the reference's half-away rounding of the
+// exact h = S / lambda_w (kernels.py:145-146, 253-268).
+// ---------------------------------------------------------------------------
+constexpr double kRecSmall = 1e-3;
+#ifndef NBX_REC_UNROLL
+#define NBX_REC_UNROLL 4
+#endif
+constexpr int kRecUnroll = NBX_REC_UNROLL;
+constexpr uint32_t kRecSmallHi = 0x3F50624Du;  // high word of 1e-3: |x| < 1e-3 <=> hi(|x|) < this (about)
+
+struct Phasor {
+    double re, im;
+};
+
+__device__ __forceinline__ void rotate(Phasor& z, const Phasor& r) {
+    const double re = __fma_rn(z.re, r.re, -(z.im * r.im));
+    const double im = __fma_rn(z.re, r.im, z.im * r.re);
+    z.re = re;
+    z.im = im;
+}
+
+__device__ __forceinline__ Phasor phasor(double x) {  // e^{i pi x}
+    Phasor z;
+    sincospi(x, &z.im, &z.re);
+    return z;
+}
+
+struct AxisRec {
+    Phasor den, num, rden, rnum;  // current e^{i pi h}, e^{i pi N h}; per-channel rotations
+};
+
+__device__ __forceinline__ AxisRec axis_rec(double S, double iv0, double delta, double N) {
+    AxisRec a;
+    const double h0 = S * iv0;
+    const double t0 = h0 - rint(h0);     // exact; e^{i pi t0} = +-e^{i pi h0}
+    a.den = phasor(t0);
+    a.num = phasor(N * t0);              // +-e^{i pi N h0} (N n0 is an integer)
+    const double d = S * delta;
+    a.rden = phasor(d);
+    a.rnum = phasor(N * d);
+    return a;
+}
+
+__device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu; }
+
+// One channel from the three axes' current phasors: w F^2 F_latt^2.
+__device__ __forceinline__ double rec_channel(const SpotsParams& P, const double* __restrict__ tab, int l0,
+                                              double2 c, double Sa, double Sb, double Sc, const Phasor& ad,
+                                              const Phasor& an, const Phasor& bd, const Phasor& bn,
+                                              const Phasor& cd, const Phasor& cn) {
+    const double ha = Sa * c.x, hb = Sb * c.x, hc = Sc * c.x;  // kernels.py:257-260
+    const int ia = __double2int_rz(ha + copysign(0.5, ha));      // round half away (kernels.py:145-146)
+    const int ib = __double2int_rz(hb + copysign(0.5, hb));
+    const int ic = __double2int_rz(hc + copysign(0.5, hc));
+    double nn = (an.im * bn.im) * cn.im;
+    double dd = (ad.im * bd.im) * cd.im;
+    if (min(min(abs_hi(ad.im), abs_hi(bd.im)), abs_hi(cd.im)) < kRecSmallHi) {
+        // near a Bragg plane: the exact reduced-phase form (both carry 1/pi^3: same ratio)
+        const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
+        const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
+        const AxisF64 e = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
+        nn = (a.num * b.num) * e.num;
+        dd = (a.den * b.den) * e.den;
+    }
+    const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+    return (__ldg(tab + (ia * P.sH + ib * P.sK + ic - l0)) * c.y) * (ratio * ratio);
+}
+
+__device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const double2* __restrict__ sch,
+                                                     const RunF64* __restrict__ sru, double Sa, double Sb,
+                                                     double Sc) {
+    const double* __restrict__ tab = static_cast<const double*>(P.table);
+    const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
+    double acc = 0.0;
+    for (int ri = 0; ri < P.n_runs; ++ri) {
+        const RunF64 run = sru[ri];
+        AxisRec A = axis_rec(Sa, run.iv0, run.delta, P.n_cells_d[0]);
+        AxisRec B = axis_rec(Sb, run.iv0, run.delta, P.n_cells_d[1]);
+        AxisRec C = axis_rec(Sc, run.iv0, run.delta, P.n_cells_d[2]);
+#pragma unroll kRecUnroll
+        for (int w = run.begin; w < run.end; ++w) {
+            acc += rec_channel(P, tab, l0, sch[w], Sa, Sb, Sc, A.den, A.num, B.den, B.num, C.den, C.num);
+            rotate(A.den, A.rden);
+            rotate(A.num, A.rnum);
+            rotate(B.den, B.rden);
+            rotate(B.num, B.rnum);
+            rotate(C.den, C.rden);
+            rotate(C.num, C.rnum);
+        }
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path, 2 = FP64 path with
+// the channel recurrence (sincg only).
 // ---------------------------------------------------------------------------
 template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
 __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : NBX_MIN_BLOCKS_F64) spots_kernel(const SpotsParams P) {
@@ -286,6 +393,10 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
         double2* s = reinterpret_cast<double2*>(smem_raw);
         const double2* g = static_cast<const double2*>(P.chan);
         for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
+        if constexpr (COMPUTE == 2) {
+            RunF64* r = reinterpret_cast<RunF64*>(smem_raw + 16 * P.n_src);
+            for (int i = tid; i < P.n_runs; i += kBlockX * kBlockY) r[i] = P.runs[i];
+        }
     }
     __syncthreads();
 
@@ -342,6 +453,12 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
                         sub += domain_sum_f32<SHAPE, WIDE, PDEG>(
                             P, reinterpret_cast<const ChunkF32*>(smem_raw),
                             reinterpret_cast<const float4*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
+                    } else if constexpr (COMPUTE == 2) {
+                        const double2* sch = reinterpret_cast<const double2*>(smem_raw);
+                        double a = domain_sum_f64_rec(P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src),
+                                                      Sa, Sb, Sc);
+                        if (!isfinite(a)) a = channel_sum_f64<0, true>(P, sch, Sa, Sb, Sc);  // limit branch
+                        sub += a;
                     } else {
                         sub += domain_sum_f64<SHAPE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
                     }
@@ -480,11 +597,16 @@ static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cu
     }
 }
 
-// compute: 0 FP64, 1 FP32, 2 FP32 with the degree-4 (ulp-grade) polynomial, sincg only
+// compute: 0 FP64, 1 FP32, 2 FP32 with the degree-4 (ulp-grade) polynomial, sincg only,
+// 4 FP64 with the channel recurrence (sincg only)
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st) {
     if (compute == 0) {
         const size_t smem = (size_t)P.n_src * 16;
         return launch_shape<0, false>(P, shape, smem, st);
+    }
+    if (compute == 4) {  // FP64 channel recurrence (sincg)
+        const size_t smem = (size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64);
+        return launch_t<2, 0, false, kPolyF32>(P, smem, st);
     }
     const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 16;  // n_src = channel pairs
     if (compute == 2 && shape == 0)

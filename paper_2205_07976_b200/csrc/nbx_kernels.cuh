@@ -32,6 +32,13 @@ struct ChunkF32 {
     int32_t begin, end;
 };
 
+// FP64 path, channel-recurrence variant: sorted channels [begin, end) whose
+// 1/lambda are an arithmetic progression iv0 + k*delta (to 1e-14 in phase).
+struct RunF64 {
+    double iv0, delta;
+    int32_t begin, end;
+};
+
 // Everything the spot kernel reads.  All pointers are device pointers.
 struct SpotsParams {
     const DevPanel* panels;
@@ -72,6 +79,9 @@ struct SpotsParams {
     int32_t bg_points;             // 0: no background
     double bg_scale;               // r_e^2 fluence thickness_factor / sum(w)
     unsigned long long* fault_bg;  // background stage's lowest non-finite pixel
+    const RunF64* runs;            // FP64 recurrence variant: uniform channel runs (sorted channels)
+    int32_t n_runs;
+    int32_t pad4;
 };
 
 }  // namespace nbx

@@ -131,11 +131,12 @@ struct BgBufs {
 struct Plan {
     Ctx* ctx = nullptr;
     int compute = 0;
-    int kernel_variant = 0;  // 0 FP64, 1 FP32, 2 FP32 with the degree-4 polynomial (NBX_FP32_POLY=4)
+    int kernel_variant = 0;  // 0 FP64, 1 FP32, 2 FP32 with the degree-4 polynomial (NBX_FP32_POLY=4),
+                             // 4 FP64 with the channel recurrence
     int shape = 0;
     bool wide = false;
     nbx::SpotsParams P{};
-    DevBuf panels, bases, chan, chunks, table;
+    DevBuf panels, bases, chan, chunks, table, runs;
     HostBuf host_table;       // pinned staging of the F^2 grid
     BgBufs bg;
     bool uniform_panels = true;  // every panel has the same (slow, fast): row bands are 2-D copies
@@ -520,13 +521,57 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells_alloc * sizeof(float),
                                 cudaMemcpyHostToDevice));
         } else {
+            // Channel-recurrence variant (sincg): channels sorted by 1/lambda and cut into
+            // runs whose 1/lambda are an arithmetic progression to within 1e-14 of phase
+            // (|S (iv_k - iv_0 - k delta)| <= 1e-14 for every reachable S); used when the
+            // runs are long enough to amortise their per-run anchors.
+            std::vector<int> order(n_src);
+            std::vector<double> iv(n_src);
+            for (int i = 0; i < n_src; ++i) {
+                order[i] = i;
+                iv[i] = 1.0 / d->wavelengths[sb + i];  // kernels.py:257
+            }
+            std::vector<nbx::RunF64> runs;
+            const char* rev = std::getenv("NBX_FP64_REC");
+            if (d->shape == NBX_SHAPE_SINCG && !(rev && std::atoi(rev) == 0) && n_src >= 2) {
+                std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return iv[x] < iv[y]; });
+                int b = 0;
+                while (b < n_src) {
+                    int e = std::min(n_src, b + 128);
+                    for (;;) {
+                        const int len = e - b;
+                        double delta = len > 1 ? (iv[order[e - 1]] - iv[order[b]]) / (double)(len - 1) : 0.0;
+                        double dev = 0.0;
+                        for (int k = 0; k < len; ++k)
+                            dev = std::max(dev, std::fabs(iv[order[b + k]] - iv[order[b]] - (double)k * delta));
+                        if (len == 1 || dev * smax <= 1e-14) {
+                            runs.push_back(nbx::RunF64{iv[order[b]], delta, b, e});
+                            break;
+                        }
+                        e = b + len / 2;
+                    }
+                    b = e;
+                }
+                if ((int64_t)runs.size() * 8 > n_src) {  // mean run shorter than 8: direct kernel
+                    runs.clear();
+                    for (int i = 0; i < n_src; ++i) order[i] = i;
+                }
+            }
             std::vector<double> ch(2 * (size_t)n_src);
             for (int i = 0; i < n_src; ++i) {
-                ch[2 * i + 0] = 1.0 / d->wavelengths[sb + i];
-                ch[2 * i + 1] = d->weights[sb + i];
+                ch[2 * i + 0] = iv[order[i]];
+                ch[2 * i + 1] = d->weights[sb + order[i]];
             }
             plan->chan.ensure(ch.size() * sizeof(double));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice));
+            if (!runs.empty()) {
+                plan->kernel_variant = 4;
+                plan->runs.ensure(runs.size() * sizeof(nbx::RunF64));
+                NBX_CUDA(cudaMemcpy(plan->runs.p, runs.data(), runs.size() * sizeof(nbx::RunF64),
+                                    cudaMemcpyHostToDevice));
+                P.runs = static_cast<const nbx::RunF64*>(plan->runs.p);
+                P.n_runs = (int32_t)runs.size();
+            }
             plan->table.ensure(cells * sizeof(double));
             NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells * sizeof(double), cudaMemcpyHostToDevice));
         }
@@ -570,6 +615,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         }
         I.compute = compute;
         I.table_kind = plan->wide ? 1 : 0;
+        I.channel_runs = P.n_runs;
         I.scale = plan->scale;
         return plan;
     } catch (...) {

@@ -235,9 +235,10 @@ def test_multi_panel_equals_single_panels(gpu):
         assert np.array_equal(single, stacked[i])
 
 
-def test_channel_shards_reduce_to_whole(gpu):
+def test_channel_shards_reduce_to_whole(gpu, monkeypatch):
     from paper_2205_07976_b200 import _native as N
 
+    monkeypatch.setenv("NBX_FP64_REC", "0")  # same (direct) kernel for the shards and the whole
     ctx = roi_ctx()
     whole = run(ctx, "f64").data
     plan_all = SpotsPlan(ctx)
@@ -245,6 +246,45 @@ def test_channel_shards_reduce_to_whole(gpu):
     for lo, hi in ((0, 3), (3, 8)):
         SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=0.0).run(raw, mode=N.OUT_RAW_F64)
     np.testing.assert_allclose(raw * plan_all.scale, whole, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_fp64_channel_recurrence_matches_direct_kernel(gpu, monkeypatch, seed):
+    """The FP64 channel recurrence (uniform 1/lambda runs, nbx_kernels.cu:domain_sum_f64_rec)
+    against the direct per-channel FP64 kernel on an LS49 ROI through the direct beam and
+    one at high resolution: 100 channels x 50 domains, per-pixel within 1e-10 of the image
+    maximum, total and every spot within 1e-11."""
+    from paper_2205_07976_b200 import _native as N
+
+    for r0 in (1888, 40):
+        panel = synthetic.roi(synthetic.rayonix_panel(), r0, r0, 64, 64)
+        ctx = synthetic.ls49_context(synthetic.SEED + seed, panel=panel, compute="fp64")
+        rec_plan = SpotsPlan(ctx)
+        assert rec_plan.info.channel_runs >= 1
+        rec = np.zeros(rec_plan.n_pixels)
+        rec_plan.run(rec, mode=N.OUT_F64)
+        monkeypatch.setenv("NBX_FP64_REC", "0")
+        direct_plan = SpotsPlan(ctx)
+        assert direct_plan.info.channel_runs == 0
+        direct = np.zeros(direct_plan.n_pixels)
+        direct_plan.run(direct, mode=N.OUT_F64)
+        monkeypatch.delenv("NBX_FP64_REC")
+        m = parity.metrics(rec, direct, panel.dims)
+        assert m["total"] < 1e-11 and m["spot"] < 1e-11, m
+        assert m["pix_abs_over_max"] < 1e-10, m
+
+
+def test_nonuniform_spectrum_uses_direct_fp64_kernel(gpu):
+    rng = np.random.default_rng(7)
+    wl = np.sort(rng.uniform(1.70, 1.76, 12))
+    spec = BeamSpectrum(samples=tuple((float(w), 1.0) for w in wl), fluence=1e24)
+    panel = synthetic.roi(synthetic.rayonix_panel(), 1888, 1888, 16, 16)
+    ctx = synthetic.ls49_context(panel=panel, n_domains=2, compute="fp64")
+    import dataclasses
+
+    ctx = dataclasses.replace(ctx, spectrum=spec)
+    assert SpotsPlan(ctx).info.channel_runs == 0
+    got, _ = oracle_check(ctx)
 
 
 def test_plan_runs_into_device_memory(gpu):
