@@ -36,6 +36,9 @@ namespace nbx {
 //   FP64 degree 6: max rel err 1.2e-13  (1e4 below the 1e-9 parity bar)
 //   FP64 degree 7: max rel err 2.9e-16
 // ---------------------------------------------------------------------------
+template <int V>
+constexpr int kDeg = (V == 4) ? 4 : 3;  // Q degree of an FP32 variant (see kMufuNum below)
+
 template <int DEG>
 __device__ __forceinline__ float q_sinpi_f32(float s) {
     if constexpr (DEG == 3) {
@@ -153,8 +156,8 @@ __device__ __forceinline__ AxisF32 axis_f32(float S_hi, float D, float f0, float
     const float ta = BIAS ? fabsf(a.t) + kTBiasF32 : fabsf(a.t);
     const float k = __fsub_rn(__fmaf_rn(N, ta, kMagicF32), kMagicF32);  // rint(N t)
     const float r = __fmaf_rn(N, ta, -k);
-    a.num = r * q_sinpi_f32<DEG>(r * r);
-    a.den = ta * q_sinpi_f32<DEG>(ta * ta);
+    a.num = r * q_sinpi_f32<kDeg<DEG>>(r * r);
+    a.den = ta * q_sinpi_f32<kDeg<DEG>>(ta * ta);
     return a;
 }
 
@@ -245,7 +248,10 @@ __device__ __forceinline__ f2x add2(f2x a, f2x b) {
 #ifndef NBX_NUM_MUFU
 #define NBX_NUM_MUFU 1  // 0: polynomial numerator on every FP32 variant (the pre-MUFU kernel)
 #endif
-constexpr float kSinLinear = 0.0099f;
+#ifndef NBX_SIN_LINEAR
+#define NBX_SIN_LINEAR 0.0099f
+#endif
+constexpr float kSinLinear = NBX_SIN_LINEAR;
 __device__ __forceinline__ float sin_approx_f32(float x) {
     float y;
     asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -279,8 +285,13 @@ struct AxisF32x2 {
 // error <= x^2/6 = 1.6e-5; the compiler predicates the MUFU, no select).  The
 // numerator is then pi x the polynomial form's (which carries sin(pi r)/pi), so
 // a chunk sum is pi^6 times the reference's; domain_sum_f32 rescales it.
-template <int DEG>
-constexpr bool kMufuNum = (DEG == 3) && (NBX_NUM_MUFU != 0);
+// FP32 variants (the DEG template argument of the FP32 helpers):
+//   3: degree-3 Q, MUFU numerator (the fast default);
+//   4: degree-4 Q, polynomial numerator ("ulp-grade", NBX_FP32_POLY=4);
+//   5: degree-3 Q, polynomial numerator (chosen when few samples per pixel would
+//      leave MUFU's absolute error un-averaged, e.g. one channel x one domain).
+template <int V>
+constexpr bool kMufuNum = (V == 3) && (NBX_NUM_MUFU != 0);
 
 // Unbiased (hot-loop) axis for two channels: the same arithmetic as axis_f32
 // without |t| (signs drop out of the squared ratio) and without the bias
@@ -303,9 +314,9 @@ __device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x
     } else {
         const f2x nk = fma2(fma2(N, t, M), neg1, M);  // -rint(N t)
         const f2x r = fma2(N, t, nk);                 // N t - rint(N t)
-        a.num = mul2(r, q_sinpi_f32x2<DEG>(mul2(r, r)));
+        a.num = mul2(r, q_sinpi_f32x2<kDeg<DEG>>(mul2(r, r)));
     }
-    a.den = mul2(t, q_sinpi_f32x2<DEG>(mul2(t, t)));
+    a.den = mul2(t, q_sinpi_f32x2<kDeg<DEG>>(mul2(t, t)));
     return a;
 }
 

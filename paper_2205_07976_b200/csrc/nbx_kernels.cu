@@ -597,8 +597,9 @@ static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cu
     }
 }
 
-// compute: 0 FP64, 1 FP32, 2 FP32 with the degree-4 (ulp-grade) polynomial, sincg only,
-// 4 FP64 with the channel recurrence (sincg only)
+// compute: 0 FP64, 1 FP32 (MUFU numerator), 2 FP32 with the degree-4 (ulp-grade) polynomial,
+// 5 FP32 degree-3 with the polynomial numerator (both sincg only), 4 FP64 with the channel
+// recurrence (sincg only)
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st) {
     if (compute == 0) {
         const size_t smem = (size_t)P.n_src * 16;
@@ -611,6 +612,8 @@ cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide
     const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 16;  // n_src = channel pairs
     if (compute == 2 && shape == 0)
         return wide ? launch_t<1, 0, true, 4>(P, smem, st) : launch_t<1, 0, false, 4>(P, smem, st);
+    if (compute == 5 && shape == 0)
+        return wide ? launch_t<1, 0, true, 5>(P, smem, st) : launch_t<1, 0, false, 5>(P, smem, st);
     return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);
 }
 

@@ -131,7 +131,8 @@ struct BgBufs {
 struct Plan {
     Ctx* ctx = nullptr;
     int compute = 0;
-    int kernel_variant = 0;  // 0 FP64, 1 FP32, 2 FP32 with the degree-4 polynomial (NBX_FP32_POLY=4),
+    int kernel_variant = 0;  // 0 FP64, 1 FP32 (MUFU numerator), 2 FP32 with the degree-4 polynomial
+                             // (NBX_FP32_POLY=4), 5 FP32 degree 3 with the polynomial numerator,
                              // 4 FP64 with the channel recurrence
     int shape = 0;
     bool wide = false;
@@ -376,6 +377,18 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         const std::vector<nbx::DevPanel> hp = make_panels(d, &max_slow, &max_fast, &off, &sub_steps);
         plan->n_pixels = off;
         plan->steps = sub_steps * (int64_t)n_src * d->n_domains;
+        if (plan->kernel_variant == 1 && d->shape == NBX_SHAPE_SINCG) {
+            // MUFU.SIN's ~1e-6 absolute error averages out over the many (channel, domain,
+            // sub-pixel) samples of a pixel; with few samples per pixel (the C1 toy: one
+            // channel x one domain, side lobes sampled one point per pixel) take the
+            // polynomial numerator instead.  NBX_FP32_NUM=mufu|poly forces either.
+            const char* nev = std::getenv("NBX_FP32_NUM");
+            const double per_pixel = off > 0 ? (double)plan->steps / (double)off : 0.0;
+            bool poly = per_pixel < 256.0;
+            if (nev && std::strcmp(nev, "mufu") == 0) poly = false;
+            if (nev && std::strcmp(nev, "poly") == 0) poly = true;
+            if (poly) plan->kernel_variant = 5;
+        }
         plan->uniform_panels = true;
         for (const auto& q : hp) plan->uniform_panels &= (q.slow == max_slow && q.fast == max_fast);
 

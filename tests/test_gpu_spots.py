@@ -73,6 +73,18 @@ def test_fp32_path_matches_reference(gpu, name):
     assert m["total"] < FP32_TOL and m["spot"] < FP32_TOL, m
 
 
+@pytest.mark.parametrize("numerator", ["mufu", "poly"])
+@pytest.mark.parametrize("name", ["c1_toy", "triclinic_pol_2wl", "ls49_centre"])
+def test_fp32_numerator_variants_match_reference(gpu, monkeypatch, name, numerator):
+    """Both FP32 numerators (MUFU.SIN on the XU pipe / degree-3 polynomial) on any input,
+    whichever the plan would pick by samples per pixel (nbx_runtime.cu:build_plan)."""
+    monkeypatch.setenv("NBX_FP32_NUM", numerator)
+    case = parity.load(name)
+    got = run(parity.context(case, "fp32"), "f32").data
+    m = parity.metrics(got, case["ref_f64"], dims(case))
+    assert m["total"] < FP32_TOL and m["spot"] < FP32_TOL, m
+
+
 # ---- the reference's own kernel tests, pointed at this implementation (test_kernels.py:99-246) ----
 
 def small_panel():
