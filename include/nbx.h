@@ -143,6 +143,10 @@ typedef struct nbx_plan_info_t {
 
 int nbx_version(void);
 
+/* sizeof the ABI structs as compiled into the library, for bindings to check their
+ * mirrors: 0 nbx_panel, 1 nbx_spots_desc, 2 nbx_plan_info_t (0 for anything else). */
+int64_t nbx_struct_size(int which);
+
 /* Per-device context: stream, scratch, last error.  NULL on failure (no GPU). */
 void* nbx_ctx_create(int device);
 void nbx_ctx_destroy(void* ctx);

@@ -29,6 +29,7 @@ EXPORTS = (
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
     "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak", "nbx_background",
     "nbx_fault_stage", "nbx_campaign", "nbx_crc32", "nbx_image_stats", "nbx_image_histogram",
+    "nbx_struct_size",
 )
 
 

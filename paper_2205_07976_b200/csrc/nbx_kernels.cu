@@ -79,7 +79,10 @@ constexpr int kPairUnroll = NBX_PAIR_UNROLL;  // channel pairs per FP32 loop ite
 #define NBX_MIN_BLOCKS_F64 2
 #endif
 constexpr int kBlockX = 32;
-constexpr int kBlockY = 8;
+#ifndef NBX_BLOCK_Y
+#define NBX_BLOCK_Y 8
+#endif
+constexpr int kBlockY = NBX_BLOCK_Y;
 constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
 constexpr int kPolyF64 = 6;  // FP64 Q(s) degree (rel err 1.2e-13)
 constexpr int kNewtonF64 = 1;

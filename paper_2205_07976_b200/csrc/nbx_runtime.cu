@@ -837,6 +837,15 @@ extern "C" {
 
 int nbx_version(void) { return NBX_VERSION; }
 
+int64_t nbx_struct_size(int which) {
+    switch (which) {
+        case 0: return (int64_t)sizeof(nbx_panel);
+        case 1: return (int64_t)sizeof(nbx_spots_desc);
+        case 2: return (int64_t)sizeof(nbx_plan_info_t);
+        default: return 0;
+    }
+}
+
 void* nbx_ctx_create(int device) {
     try {
         int n = 0;

@@ -106,3 +106,26 @@ def test_crc32_matches_zlib(lib):
     for n in (0, 1, 7, 8, 9, 4096, 100003):
         b = np.random.default_rng(n).integers(0, 256, n, dtype=np.uint8)
         assert lib.nbx_crc32(0, b.ctypes.data, n) == zlib.crc32(b.tobytes())
+
+
+def test_struct_mirrors_match_the_library(lib):
+    """The ctypes mirrors (_native.py) have the sizes the library was compiled with."""
+    lib.nbx_struct_size.restype = C.c_int64
+    assert lib.nbx_struct_size(0) == C.sizeof(_native.Panel)
+    assert lib.nbx_struct_size(1) == C.sizeof(_native.SpotsDesc)
+    assert lib.nbx_struct_size(2) == C.sizeof(_native.PlanInfo)
+    assert lib.nbx_struct_size(7) == 0
+
+
+def test_integration_doc_binding_matches_the_library(lib):
+    """The self-contained ctypes binding shown in INTEGRATION.md section 2 is ABI-correct."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = text.split("## 2. Raw C ABI", 1)[1].split("```python", 1)[1].split("```", 1)[0]
+    structs = block.split("lib.nbx_struct_size.restype", 1)[0]  # imports + the two Structure classes
+    ns = {}
+    exec(compile(structs.replace('lib = C.CDLL("/path/to/paper_2205_07976_b200/_lib/libnbx.so")', ""),
+                 "INTEGRATION.md", "exec"), ns)
+    lib.nbx_struct_size.restype = C.c_int64
+    assert lib.nbx_struct_size(0) == C.sizeof(ns["Panel"])
+    assert lib.nbx_struct_size(1) == C.sizeof(ns["Desc"])
+    assert [f[0] for f in ns["Desc"]._fields_] == [f[0] for f in _native.SpotsDesc._fields_]
