@@ -34,6 +34,11 @@ sys.path.insert(0, str(ROOT))
 METRIC = "images/s and Gsteps/s (pixel×source×mosaic×subpixel) at 1/2/4/8 B200"
 WORKLOAD = "C2 LS49-shape image: 3840x3840 Rayonix-like, 100 energy channels, 50 mosaic domains, oversample 1"
 STEP_INSTR = 126  # FP-pipe instructions per step, SURVEY §8 D1 (FMA = 1)
+# What the implementation actually issues per step on its bounding pipe, counted in the
+# SASS of the hot loop (tools/sass_loop.py), by nbx_plan_info_t.kernel_variant:
+#   (pipe, pipe lane-ops per step, lanes per SM per clock of that pipe)
+IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 40, 64)}
+SMS = 148
 
 
 def parse():
@@ -280,6 +285,14 @@ def run_ours(args):
                               "peak = live FMA probe (nbx_probe_fma_peak) on this GPU"},
         "clocks": clocks.summary(),
     }
+    # the implementation's own pipe utilisation (frac above is against the fixed 126-op figure)
+    pipe, ops, lanes = IMPL_OPS.get(plans[0].info.kernel_variant, (None, None, None))
+    clk = result["clocks"].get("sm_mhz") or 1965.0
+    if ops:
+        result["roofline"]["implementation"] = {
+            "kernel_variant": plans[0].info.kernel_variant, "pipe": pipe, "pipe_ops_per_step": ops,
+            "pipe_frac": gsteps / world * 1e9 * ops / (SMS * lanes * clk * 1e6),
+            "basis": "steps/s x SASS-counted bounding-pipe lane-ops per step / (148 SMs x lanes x SM clock)"}
 
     if not args.no_extras:
         # e2e: the public API with host buffers, descriptor upload and image download inside the timed region

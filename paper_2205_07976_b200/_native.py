@@ -61,7 +61,7 @@ class PlanInfo(C.Structure):
     _fields_ = [
         ("n_pixels", C.c_int64), ("steps", C.c_int64), ("table_cells", C.c_int64),
         ("table_lo", C.c_int32 * 3), ("table_dim", C.c_int32 * 3), ("compute", C.c_int32),
-        ("table_kind", C.c_int32), ("scale", C.c_double), ("channel_runs", C.c_int32), ("reserved", C.c_int32),
+        ("table_kind", C.c_int32), ("scale", C.c_double), ("channel_runs", C.c_int32), ("kernel_variant", C.c_int32),
     ]
 
 

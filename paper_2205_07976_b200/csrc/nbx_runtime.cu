@@ -629,6 +629,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         I.compute = compute;
         I.table_kind = plan->wide ? 1 : 0;
         I.channel_runs = P.n_runs;
+        I.kernel_variant = plan->kernel_variant;
         I.scale = plan->scale;
         return plan;
     } catch (...) {
