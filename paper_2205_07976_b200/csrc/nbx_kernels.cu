@@ -276,72 +276,76 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 // FP64 path, channel recurrence (sincg, spectra whose 1/lambda form arithmetic
 // progressions -- every BASELINE config: E_j = E_0 + j dE).  Along a run the
 // phase of each axis advances by Delta = S delta per channel, so
-//     z_den = e^{i pi h_w}  and  z_num = e^{i pi N h_w}
-// are complex rotations (2 DMUL + 2 DFMA each) instead of two degree-6
-// polynomials and a range reduction; sin(pi h) and sin(pi N h) are their
-// imaginary parts (signs drop out of F_latt^2).  Anchors and rotation factors
-// come from sincospi once per (pixel, sub-pixel, domain, run).  The rotations
-// drift by ~k ulp after k channels, i.e. an ABSOLUTE error of ~1e-14 in each
-// sine: harmless except where the denominator itself is small, so a channel
-// with any |sin(pi h)| < kRecSmall is evaluated directly from the exact
-// reduced phase t = h - n (axis_f64) -- per-step relative error stays below
-// ~3e-11.  The Fhkl index keeps the reference's half-away rounding of the
-// exact h = S / lambda_w (kernels.py:145-146, 253-268).
+//     sin(pi h_k)  and  sin(pi N h_k),  h_k = h_0 + k Delta,
+// are sine sequences of fixed step, advanced by Reinsch's form of the
+// three-term recurrence (well conditioned for small steps):
+//     d_{k+1} = d_k - alpha s_k,   s_{k+1} = s_k + d_{k+1},   alpha = 4 sin^2(theta/2)
+// -- one DFMA + one DADD per sine per channel instead of a range reduction and
+// a degree-6 polynomial.  Steps are reduced mod 1 first (sin^2 has period 1 in
+// h and in N h), so |theta| <= pi/2.  Anchors come from sincospi once per
+// (pixel, sub-pixel, domain, run).  The recurrences drift by ~k ulp, an
+// ABSOLUTE error of ~1e-14 in each sine: harmless except where the
+// denominator itself is small, so a channel with any |sin(pi h)| < 1e-3 is
+// evaluated directly from the exact reduced phase t = h - n (axis_f64) --
+// per-step relative error stays below ~1e-11.  The Fhkl index keeps the
+// reference's half-away rounding of the exact h = S / lambda_w
+// (kernels.py:145-146, 253-268).
 // ---------------------------------------------------------------------------
-constexpr double kRecSmall = 1e-3;
 #ifndef NBX_REC_UNROLL
 #define NBX_REC_UNROLL 4
 #endif
 constexpr int kRecUnroll = NBX_REC_UNROLL;
-constexpr uint32_t kRecSmallHi = 0x3F50624Du;  // high word of 1e-3: |x| < 1e-3 <=> hi(|x|) < this (about)
+constexpr uint32_t kRecSmallHi = 0x3F50624Du;  // high word of 1e-3: |x| < ~1e-3 <=> hi(|x|) < this
 
-struct Phasor {
-    double re, im;
+struct SineSeq {
+    double s, d, a;  // current sine, s_k - s_{k-1}, alpha
 };
 
-__device__ __forceinline__ void rotate(Phasor& z, const Phasor& r) {
-    const double re = __fma_rn(z.re, r.re, -(z.im * r.im));
-    const double im = __fma_rn(z.re, r.im, z.im * r.re);
-    z.re = re;
-    z.im = im;
+// sin(pi (x0 + k y)) for k = 0, 1, ... (up to a sign flip per step, which squares away).
+__device__ __forceinline__ SineSeq sine_seq(double x0, double y) {
+    y -= rint(y);
+    double s0, c0, sg, kp;
+    sincospi(x0, &s0, &c0);
+    sincospi(0.5 * y, &sg, &kp);
+    SineSeq q;
+    q.s = s0;
+    q.d = 2.0 * sg * __fma_rn(s0, sg, c0 * kp);  // s_0 - s_{-1}
+    q.a = 4.0 * sg * sg;
+    return q;
 }
 
-__device__ __forceinline__ Phasor phasor(double x) {  // e^{i pi x}
-    Phasor z;
-    sincospi(x, &z.im, &z.re);
-    return z;
+__device__ __forceinline__ void advance(SineSeq& q) {
+    q.d = __fma_rn(-q.a, q.s, q.d);
+    q.s += q.d;
 }
 
 struct AxisRec {
-    Phasor den, num, rden, rnum;  // current e^{i pi h}, e^{i pi N h}; per-channel rotations
+    SineSeq den, num;  // sin(pi h_k), sin(pi N h_k)
 };
 
 __device__ __forceinline__ AxisRec axis_rec(double S, double iv0, double delta, double N) {
     AxisRec a;
     const double h0 = S * iv0;
-    const double t0 = h0 - rint(h0);     // exact; e^{i pi t0} = +-e^{i pi h0}
-    a.den = phasor(t0);
-    a.num = phasor(N * t0);              // +-e^{i pi N h0} (N n0 is an integer)
+    const double t0 = h0 - rint(h0);  // exact
     const double d = S * delta;
-    a.rden = phasor(d);
-    a.rnum = phasor(N * d);
+    a.den = sine_seq(t0, d);
+    a.num = sine_seq(N * t0, N * d);  // N n0 is an integer
     return a;
 }
 
 __device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu; }
 
-// One channel from the three axes' current phasors: w F^2 F_latt^2.
+// One channel from the three axes' current sines: w F^2 F_latt^2.
 __device__ __forceinline__ double rec_channel(const SpotsParams& P, const double* __restrict__ tab, int l0,
-                                              double2 c, double Sa, double Sb, double Sc, const Phasor& ad,
-                                              const Phasor& an, const Phasor& bd, const Phasor& bn,
-                                              const Phasor& cd, const Phasor& cn) {
+                                              double2 c, double Sa, double Sb, double Sc, double ad, double an,
+                                              double bd, double bn, double cd, double cn) {
     const double ha = Sa * c.x, hb = Sb * c.x, hc = Sc * c.x;  // kernels.py:257-260
     const int ia = __double2int_rz(ha + copysign(0.5, ha));      // round half away (kernels.py:145-146)
     const int ib = __double2int_rz(hb + copysign(0.5, hb));
     const int ic = __double2int_rz(hc + copysign(0.5, hc));
-    double nn = (an.im * bn.im) * cn.im;
-    double dd = (ad.im * bd.im) * cd.im;
-    if (min(min(abs_hi(ad.im), abs_hi(bd.im)), abs_hi(cd.im)) < kRecSmallHi) {
+    double nn = (an * bn) * cn;
+    double dd = (ad * bd) * cd;
+    if (min(min(abs_hi(ad), abs_hi(bd)), abs_hi(cd)) < kRecSmallHi) {
         // near a Bragg plane: the exact reduced-phase form (both carry 1/pi^3: same ratio)
         const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
         const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
@@ -366,13 +370,14 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
         AxisRec C = axis_rec(Sc, run.iv0, run.delta, P.n_cells_d[2]);
 #pragma unroll kRecUnroll
         for (int w = run.begin; w < run.end; ++w) {
-            acc += rec_channel(P, tab, l0, sch[w], Sa, Sb, Sc, A.den, A.num, B.den, B.num, C.den, C.num);
-            rotate(A.den, A.rden);
-            rotate(A.num, A.rnum);
-            rotate(B.den, B.rden);
-            rotate(B.num, B.rnum);
-            rotate(C.den, C.rden);
-            rotate(C.num, C.rnum);
+            acc += rec_channel(P, tab, l0, sch[w], Sa, Sb, Sc, A.den.s, A.num.s, B.den.s, B.num.s, C.den.s,
+                               C.num.s);
+            advance(A.den);
+            advance(A.num);
+            advance(B.den);
+            advance(B.num);
+            advance(C.den);
+            advance(C.num);
         }
     }
     return acc;
