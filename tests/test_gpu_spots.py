@@ -286,6 +286,33 @@ def test_fp64_channel_recurrence_matches_direct_kernel(gpu, monkeypatch, seed):
         assert m["pix_abs_over_max"] < 1e-10, m
 
 
+def test_fp64_recurrence_multiple_runs_matches_direct_kernel(gpu, monkeypatch):
+    """Three uniform segments of different spacing plus a 300-channel segment (runs are
+    capped at 128): several runs per domain, ragged run ends, unsorted input order."""
+    from paper_2205_07976_b200 import _native as N
+
+    e = np.concatenate([7000.0 + 0.7 * np.arange(37), 7050.0 + 1.3 * np.arange(50), 7140.0 + 0.25 * np.arange(13),
+                        7200.0 + 0.05 * np.arange(300)])
+    rng = np.random.default_rng(11)
+    rng.shuffle(e)
+    w = rng.uniform(0.5, 1.5, e.size)
+    spec = BeamSpectrum(samples=tuple(zip((12398.419843 / e).tolist(), w.tolist())), fluence=1e24,
+                        polarization_on=True)
+    import dataclasses
+
+    panel = synthetic.roi(synthetic.rayonix_panel(), 1890, 1890, 24, 24)
+    ctx = dataclasses.replace(synthetic.ls49_context(panel=panel, n_domains=3, compute="fp64"), spectrum=spec)
+    plan = SpotsPlan(ctx)
+    assert plan.info.channel_runs >= 6
+    rec = np.zeros(plan.n_pixels)
+    plan.run(rec, mode=N.OUT_F64)
+    monkeypatch.setenv("NBX_FP64_REC", "0")
+    direct = np.zeros(plan.n_pixels)
+    SpotsPlan(ctx).run(direct, mode=N.OUT_F64)
+    m = parity.metrics(rec, direct, panel.dims)
+    assert m["total"] < 1e-11 and m["spot"] < 1e-11 and m["pix_abs_over_max"] < 1e-10, m
+
+
 def test_nonuniform_spectrum_uses_direct_fp64_kernel(gpu):
     rng = np.random.default_rng(7)
     wl = np.sort(rng.uniform(1.70, 1.76, 12))
