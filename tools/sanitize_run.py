@@ -1,0 +1,61 @@
+"""Small runs of every kernel variant, for compute-sanitizer (memcheck / racecheck / initcheck).
+
+usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py
+Covers: FP32 MUFU / polynomial / degree-4 numerators, FP64 direct and recurrence, the
+non-grating shapes, the wide (integer) index, thickness layers + multi-panel, background
+fused into the image, the banded (pipelined) host download, add_array, noise, stats.
+"""
+import dataclasses
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+
+from paper_2205_07976_b200 import (BackgroundProfile, Detector, PixelBuffer, SpotsPlan, add_array, add_noise,
+                                   nanobragg_spots, simulate_image, synthetic)
+from paper_2205_07976_b200 import _native as N
+from paper_2205_07976_b200.io import image_histogram, image_stats
+
+WATER = BackgroundProfile(points=((0.0, 2.57), (0.07, 2.8), (0.12, 5.0), (0.3, 6.5)))
+
+
+def run(ctx, precision="f32"):
+    out = PixelBuffer.zeros(ctx.panel.dims, precision)
+    nanobragg_spots(ctx, out)
+    assert np.all(np.isfinite(out.data))
+    return out
+
+
+roi = synthetic.roi(synthetic.rayonix_panel(), 1890, 1890, 40, 36)
+for compute in ("fp32", "fp64"):
+    for nch, ndom in ((3, 2), (64, 4)):  # few samples (polynomial / direct) and many (MUFU / recurrence)
+        ctx = synthetic.ls49_context(panel=roi, n_channels=nch, n_domains=ndom, compute=compute)
+        run(ctx)
+        print(compute, nch, ndom, "variant", SpotsPlan(ctx).info.kernel_variant, flush=True)
+os.environ["NBX_FP32_POLY"] = "4"
+run(synthetic.ls49_context(panel=roi, n_channels=8, n_domains=2, compute="fp32"))
+del os.environ["NBX_FP32_POLY"]
+for shape in ("gauss", "round", "tophat"):
+    for compute in ("fp32", "fp64"):
+        run(dataclasses.replace(synthetic.ls49_context(panel=roi, n_channels=4, n_domains=2, compute=compute),
+                                shape=shape))
+# multi-panel detector with thickness layers and oversampling
+det = synthetic.jungfrau_detector(n_side=2, size=20, thickness=320e-6)
+for compute in ("fp32", "fp64"):
+    run(dataclasses.replace(synthetic.ls49_context(panel=det, n_channels=4, n_domains=2, compute=compute),
+                            oversample=2))
+# banded host download (>= 2^20 pixels), ragged last band
+big = synthetic.roi(synthetic.rayonix_panel(), 1400, 1400, 1030, 1024)
+run(synthetic.ls49_context(panel=big, n_channels=1, n_domains=1, compute="fp32"))
+# spots + background fused, add_array, noise, stats
+ctx = synthetic.ls49_context(panel=roi, n_channels=4, n_domains=2, compute="fp32")
+img = simulate_image(ctx, background=WATER)
+spots = run(ctx)
+acc = PixelBuffer.zeros(roi.dims, "f64")
+add_array(acc, spots)
+add_noise(spots, seed=5)
+image_stats(img)
+image_histogram(img, 16, (0.0, float(img.data.max()) + 1.0))
+print("sanitize run complete", flush=True)
