@@ -285,7 +285,7 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 // h and in N h), so |theta| <= pi/2.  Anchors come from sincospi once per
 // (pixel, sub-pixel, domain, run).  The recurrences drift by ~k ulp, an
 // ABSOLUTE error of ~1e-14 in each sine: harmless except where the
-// denominator itself is small, so a channel with any |sin(pi h)| < 1e-3 is
+// denominator itself is small, so a channel with any |sin(pi h)| < 1e-4 is
 // evaluated directly from the exact reduced phase t = h - n (axis_f64) --
 // per-step relative error stays below ~1e-11.  The Fhkl index keeps the
 // reference's half-away rounding of the exact h = S / lambda_w
@@ -295,7 +295,10 @@ __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const dou
 #define NBX_REC_UNROLL 4
 #endif
 constexpr int kRecUnroll = NBX_REC_UNROLL;
-constexpr uint32_t kRecSmallHi = 0x3F50624Du;  // high word of 1e-3: |x| < ~1e-3 <=> hi(|x|) < this
+#ifndef NBX_REC_SMALL_HI
+#define NBX_REC_SMALL_HI 0x3F1A36E2u  // high word of 1e-4
+#endif
+constexpr uint32_t kRecSmallHi = NBX_REC_SMALL_HI;  // |x| < ~1e-4 <=> hi(|x|) < this
 
 struct SineSeq {
     double s, d, a;  // current sine, s_k - s_{k-1}, alpha
