@@ -351,6 +351,9 @@ def run_ours(args):
                                             "unit": "TFLOP/s", "frac": ach64 / peak64.value if peak64.value else None}}
         p64.close()
 
+    if rank == 0 and not args.no_extras and world == 1 and mode == "image":
+        result["stages"] = stage_timings(cx, N, torch, stream, ctx_for(0, args.compute), panel)
+
     if rank == 0 and not args.no_extras and world == 1:
         result["cpu_baseline"] = cpu_baseline_port(ctx_for(0, "fp64"), panel, steps_per_image, oracle)
 
@@ -360,6 +363,67 @@ def run_ours(args):
         p.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def hbm_peak_gbs() -> tuple[float, str]:
+    try:
+        v = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def stage_timings(cx, N, torch, stream, ctx, panel) -> dict:
+    """Device time of the stages around the spot kernel on the same C2 detector:
+    add_background, simulate_image's fused spots+background launch, add_array, image_stats /
+    image_histogram, Poisson noise; HBM-bound ones against the HBM peak with their algorithmic bytes."""
+    from paper_2205_07976_b200 import BackgroundProfile
+    from paper_2205_07976_b200.kernels import _bg_descriptor, describe
+
+    water = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.162, 8.0),
+                                      (0.2, 7.5), (0.25, 7.0), (0.3, 6.5), (0.35, 6.1), (0.4, 5.8), (0.45, 5.5),
+                                      (0.5, 5.2)))
+    n = panel.n_pixels
+    f32 = torch.rand(n, dtype=torch.float32, device="cuda") * 100
+    f64 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    out32 = torch.empty(n, dtype=torch.float32, device="cuda")
+    bad = N.C.c_int64(-1)
+    bg_desc = _bg_descriptor(water, panel, ctx.spectrum, 1.0)
+    img_desc = describe(ctx, background=water, thickness_factor=1.0)
+    four = (N.C.c_double * 4)()
+    counts = (N.C.c_int64 * 64)()
+    uo, oo = N.C.c_int64(0), N.C.c_int64(0)
+    lib, h = cx.lib, cx.handle
+    calls = {
+        "add_background": (lambda: lib.nbx_background(h, N.C.byref(bg_desc.c), N.OUT_F32, out32.data_ptr(), 1,
+                                                      N.C.byref(bad)), None),
+        "simulate_image_fused": (lambda: lib.nbx_spots(h, N.C.byref(img_desc.c), N.COMPUTE[ctx.compute],
+                                                       N.OUT_IMAGE_F64, f64.data_ptr(), 1, N.C.byref(bad)), None),
+        "add_array": (lambda: lib.nbx_add_array(h, N.C.c_void_p(f64.data_ptr()), N.C.c_void_p(f32.data_ptr()),
+                                                n, 1), 20 * n),
+        "image_stats": (lambda: lib.nbx_image_stats(h, N.C.c_void_p(f32.data_ptr()), n, 0, 1, four), 4 * n),
+        "image_histogram": (lambda: lib.nbx_image_histogram(h, N.C.c_void_p(f32.data_ptr()), n, 0, 1, 64, 0.0,
+                                                            100.0, counts, N.C.byref(uo), N.C.byref(oo)), 4 * n),
+        "poisson_noise": (lambda: lib.nbx_add_noise(h, N.C.c_void_p(f32.data_ptr()), N.C.c_void_p(out32.data_ptr()),
+                                                    n, 0, 7, 0, 1), 8 * n),
+    }
+    peak, peak_src = hbm_peak_gbs()
+    res = {"detector": f"C2 {panel.slow_pixels}x{panel.fast_pixels}", "hbm_peak_gbs": peak, "hbm_peak_source": peak_src}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for name, (fn, nbytes) in calls.items():
+        assert fn() == 0, name
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        row = {"ms": ms}
+        if nbytes:
+            row.update({"algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak})
+        res[name] = row
+    return res
 
 
 def cpu_baseline_port(ctx, panel, steps_per_image, oracle):

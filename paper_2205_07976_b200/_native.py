@@ -110,6 +110,7 @@ def load() -> C.CDLL:
             "nbx_image_stats": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_double)]),
             "nbx_image_histogram": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                               C.c_double, i64p, i64p, i64p]),
+            "nbx_struct_size": (C.c_int64, [C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

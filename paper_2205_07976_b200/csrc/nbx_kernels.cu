@@ -25,19 +25,22 @@ enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 
 // (_panel_geometry with oversample 1, :158-194), stol = sin(theta)/lambda per
 // source, np.interp of the profile (clamped ends), weighted mean of f_bg^2,
 // times r_e^2 fluence thickness_factor / sum(w) and Omega*pol.
+//
+// np.interp (NumPy arr_interp) with len(xp) <= len(x) precomputes
+// slope_j = (fp[j+1]-fp[j]) / (xp[j+1]-xp[j]) and returns slope_j*(x-xp[j]) + fp[j]
+// for xp[j] <= x < xp[j+1]; the host precomputes the same slopes (P.bg_fs =
+// {fp_j, slope_j}), so the device value is the same arithmetic.  The interval
+// is found by walking from the previous source's (stol moves little between
+// sources; spectra are usually sorted), not by a fresh binary search.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double interp_profile(const double* __restrict__ xp, const double* __restrict__ fp, int n,
-                                                 double x) {
-    if (x <= __ldg(xp)) return __ldg(fp);
-    if (x >= __ldg(xp + n - 1)) return __ldg(fp + n - 1);
-    int lo = 0, hi = n - 1;  // xp[lo] <= x < xp[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(xp + mid) <= x) lo = mid; else hi = mid;
-    }
-    const double x0 = __ldg(xp + lo), y0 = __ldg(fp + lo);
-    const double slope = (__ldg(fp + lo + 1) - y0) / (__ldg(xp + lo + 1) - x0);
-    return slope * (x - x0) + y0;
+__device__ __forceinline__ double interp_profile(const double* __restrict__ xp, const double2* __restrict__ fs, int n,
+                                                 double x, int& j) {
+    if (x <= __ldg(xp)) return __ldg(fs).x;
+    if (x >= __ldg(xp + n - 1)) return __ldg(fs + n - 1).x;
+    while (__ldg(xp + j + 1) <= x) ++j;  // xp[j] <= x < xp[j+1], 0 <= j <= n-2
+    while (__ldg(xp + j) > x) --j;
+    const double2 f = __ldg(fs + j);
+    return __dadd_rn(__dmul_rn(f.y, x - __ldg(xp + j)), f.x);  // NumPy: no FMA contraction
 }
 
 __device__ __forceinline__ double background_value(const SpotsParams& P, const DevPanel& pan, int sl, int f) {
@@ -56,10 +59,11 @@ __device__ __forceinline__ double background_value(const SpotsParams& P, const D
     if (P.pol_on) op *= 0.5 * (1.0 + c2t * c2t);
     const double sin_theta = sqrt(0.5 * (1.0 - c2t));
     double acc = 0.0;
+    int j = 0;
     for (int w = 0; w < P.n_bg_chan; ++w) {
         const double2 lw = __ldg(P.bg_chan + w);  // {lambda, weight}
-        const double fbg = interp_profile(P.bg_stol, P.bg_f, P.bg_points, sin_theta / lw.x);
-        acc += lw.y * (fbg * fbg);
+        const double fbg = interp_profile(P.bg_stol, P.bg_fs, P.bg_points, sin_theta / lw.x, j);
+        acc = __dadd_rn(acc, __dmul_rn(lw.y, fbg * fbg));  // acc += weights[w] * (f_bg * f_bg)
     }
     return P.bg_scale * acc * op;
 }

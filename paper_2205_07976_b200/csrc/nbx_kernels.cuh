@@ -74,7 +74,7 @@ struct SpotsParams {
     // diffuse background (kernels.py:279-312)
     const double2* bg_chan;        // {lambda, w} of every source
     const double* bg_stol;
-    const double* bg_f;
+    const double2* bg_fs;          // {f_bg, slope to the next point} per profile point
     int32_t n_bg_chan;
     int32_t bg_points;             // 0: no background
     double bg_scale;               // r_e^2 fluence thickness_factor / sum(w)

@@ -325,13 +325,20 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
     }
     B.chan.ensure(lw.size() * sizeof(double));
     NBX_CUDA(cudaMemcpy(B.chan.p, lw.data(), lw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // {f_j, slope_j}: np.interp's own precomputed slopes (same IEEE expression)
+    std::vector<double> fs(2 * (size_t)d->bg_points, 0.0);
+    for (int i = 0; i < d->bg_points; ++i) {
+        fs[2 * i] = d->bg_f[i];
+        if (i + 1 < d->bg_points)
+            fs[2 * i + 1] = (d->bg_f[i + 1] - d->bg_f[i]) / (d->bg_stol[i + 1] - d->bg_stol[i]);
+    }
     B.stol.ensure(sizeof(double) * d->bg_points);
-    B.f.ensure(sizeof(double) * d->bg_points);
+    B.f.ensure(sizeof(double) * fs.size());
     NBX_CUDA(cudaMemcpy(B.stol.p, d->bg_stol, sizeof(double) * d->bg_points, cudaMemcpyHostToDevice));
-    NBX_CUDA(cudaMemcpy(B.f.p, d->bg_f, sizeof(double) * d->bg_points, cudaMemcpyHostToDevice));
+    NBX_CUDA(cudaMemcpy(B.f.p, fs.data(), sizeof(double) * fs.size(), cudaMemcpyHostToDevice));
     P.bg_chan = static_cast<const double2*>(B.chan.p);
     P.bg_stol = static_cast<const double*>(B.stol.p);
-    P.bg_f = static_cast<const double*>(B.f.p);
+    P.bg_fs = static_cast<const double2*>(B.f.p);
     P.n_bg_chan = d->n_sources;
     P.bg_points = d->bg_points;
     P.bg_scale = d->r_e_sqr * d->fluence * d->bg_thickness_factor / wsum;  // kernels.py:299
