@@ -1,11 +1,19 @@
 // nbx_reduce.cu -- image statistics and histogram on the device (
 // image_stats / image_histogram, /root/reference/pkg/src/xtrace/kernels.py:334-430).
 //
-// Determinism: like the reference's fixed-tree reduce (execution.py:233-285),
-// the summation order depends only on n: block b sums elements
-// [b*8192, (b+1)*8192) with a fixed per-thread stride and a fixed shared-memory
-// tree, and the per-block partials are combined by one block in a fixed tree.
-// min/max are exact; counts are integers (atomics are order-free).
+// image_stats reproduces the reference's total BIT FOR BIT:
+//   * each 8192-pixel block is summed as float(np.sum(chunk, dtype=np.float64))
+//     (kernels.py:355-360), i.e. NumPy's pairwise summation of the (exactly
+//     upcast) block -- leaves of <= 128 elements with 8 strided accumulators,
+//     a power-of-two tree above them, -0.0 start for leaves shorter than 8
+//     (numpy/_core/src/umath/loops_utils.h.src, <TYPE>_pairwise_sum; a block
+//     fits NumPy's 8192-element cast buffer, so no buffering splits occur);
+//   * the block results are combined by parallel_reduce's fixed tree, which
+//     splits every span at the largest power of two strictly below its size
+//     (execution.py:227-285).
+// min/max are exact.  Full blocks are summed by 64 threads (one leaf each, the
+// block staged in shared memory); a ragged last block and the cross-block tree
+// are evaluated by one thread each with the same recursion.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -14,6 +22,8 @@ namespace nbx {
 
 constexpr int kStatsBlock = 8192;  // kernels.py:343 (_STATS_BLOCK)
 constexpr int kThreads = 256;
+constexpr int kLeaf = 128;         // NumPy PW_BLOCKSIZE
+constexpr int kLeafPad = kLeaf + 1;
 
 template <typename T>
 __device__ __forceinline__ double load_as_double(const void* p, int64_t i) {
@@ -24,47 +34,157 @@ struct Partial {
     double mn, mx, sum;
 };
 
-__device__ __forceinline__ Partial combine(Partial a, Partial b) {
-    return Partial{fmin(a.mn, b.mn), fmax(a.mx, b.mx), a.sum + b.sum};
+// NumPy's leaf: n < 8 sequential from -0.0; else 8 strided accumulators, a fixed
+// tree, then the n % 8 tail sequentially.  `at(i)` reads element i as double.
+template <typename F>
+__device__ double numpy_leaf(F at, int n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int i = 0; i < n; ++i) res += at(i);
+        return res;
+    }
+    double r0 = at(0), r1 = at(1), r2 = at(2), r3 = at(3), r4 = at(4), r5 = at(5), r6 = at(6), r7 = at(7);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+        r0 += at(i + 0);
+        r1 += at(i + 1);
+        r2 += at(i + 2);
+        r3 += at(i + 3);
+        r4 += at(i + 4);
+        r5 += at(i + 5);
+        r6 += at(i + 6);
+        r7 += at(i + 7);
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res += at(i);
+    return res;
+}
+
+// NumPy's pairwise recursion (split n/2 rounded down to a multiple of 8), iteratively.
+template <typename T>
+__device__ double numpy_pairwise(const T* a, int n) {
+    struct Frame {
+        int off, n, state;
+        double left;
+    };
+    Frame st[16];
+    int sp = 0;
+    st[0] = Frame{0, n, 0, 0.0};
+    double ret = 0.0;
+    for (;;) {
+        Frame& f = st[sp];
+        if (f.n <= kLeaf) {
+            const T* b = a + f.off;
+            ret = numpy_leaf([b](int i) { return (double)b[i]; }, f.n);
+            if (sp == 0) return ret;
+            --sp;
+            continue;
+        }
+        int n2 = f.n / 2;
+        n2 -= n2 % 8;
+        if (f.state == 0) {  // descend left
+            f.state = 1;
+            st[++sp] = Frame{f.off, n2, 0, 0.0};
+        } else if (f.state == 1) {  // left done: descend right
+            f.left = ret;
+            f.state = 2;
+            st[++sp] = Frame{f.off + n2, f.n - n2, 0, 0.0};
+        } else {  // right done
+            ret = f.left + ret;
+            if (sp == 0) return ret;
+            --sp;
+        }
+    }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) stats_blocks_kernel(const void* __restrict__ data, int64_t n,
                                                                 Partial* __restrict__ parts) {
-    __shared__ Partial sh[kThreads];
+    extern __shared__ __align__(16) unsigned char stats_smem[];
+    T* blk = reinterpret_cast<T*>(stats_smem);  // 64 leaves of 128 in padded rows (raw T, upcast on use)
+    __shared__ double leaf[kStatsBlock / kLeaf];
+    __shared__ double mn_s[kThreads], mx_s[kThreads];
     const int64_t lo = (int64_t)blockIdx.x * kStatsBlock;
-    const int64_t hi = min(n, lo + kStatsBlock);
-    Partial p{INFINITY, -INFINITY, 0.0};
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-        const double v = load_as_double<T>(data, i);
-        p = combine(p, Partial{v, v, v});
+    const int len = (int)min((int64_t)kStatsBlock, n - lo);
+    const T* src = static_cast<const T*>(data) + lo;
+    double mn = INFINITY, mx = -INFINITY;
+    for (int i = threadIdx.x; i < len; i += kThreads) {  // coalesced staging, exact upcast
+        const T raw = src[i];
+        const double v = (double)raw;
+        blk[(i / kLeaf) * kLeafPad + (i % kLeaf)] = raw;
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
     }
-    sh[threadIdx.x] = p;
+    mn_s[threadIdx.x] = mn;
+    mx_s[threadIdx.x] = mx;
     __syncthreads();
     for (int s = kThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] = combine(sh[threadIdx.x], sh[threadIdx.x + s]);
+        if (threadIdx.x < s) {
+            mn_s[threadIdx.x] = fmin(mn_s[threadIdx.x], mn_s[threadIdx.x + s]);
+            mx_s[threadIdx.x] = fmax(mx_s[threadIdx.x], mx_s[threadIdx.x + s]);
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) parts[blockIdx.x] = sh[0];
+    double sum;
+    if (len == kStatsBlock) {
+        // pairwise(8192): a perfect binary tree over 64 leaves of 128
+        if (threadIdx.x < kStatsBlock / kLeaf) {
+            const T* row = blk + threadIdx.x * kLeafPad;
+            leaf[threadIdx.x] = numpy_leaf([row](int i) { return (double)row[i]; }, kLeaf);
+        }
+        __syncthreads();
+        for (int w = kStatsBlock / kLeaf / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) leaf[threadIdx.x] = leaf[2 * threadIdx.x] + leaf[2 * threadIdx.x + 1];
+            __syncthreads();
+        }
+        sum = leaf[0];
+    } else {
+        sum = threadIdx.x == 0 ? numpy_pairwise<T>(src, len) : 0.0;  // ragged last block
+    }
+    if (threadIdx.x == 0) parts[blockIdx.x] = Partial{mn_s[0], mx_s[0], 0.0 + sum};
 }
 
-// One block folds the per-block partials: fixed strided accumulation + fixed tree.
-__global__ void __launch_bounds__(kThreads) stats_final_kernel(const Partial* __restrict__ parts, int64_t nb,
-                                                               double* __restrict__ out) {
-    __shared__ Partial sh[kThreads];
-    Partial p{INFINITY, -INFINITY, 0.0};
-    for (int64_t i = threadIdx.x; i < nb; i += kThreads) p = combine(p, parts[i]);
-    sh[threadIdx.x] = p;
-    __syncthreads();
-    for (int s = kThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] = combine(sh[threadIdx.x], sh[threadIdx.x + s]);
-        __syncthreads();
+// parallel_reduce's tree over the block partials (execution.py:227-285): a span splits
+// at the largest power of two strictly below its size; one thread, iteratively.
+__global__ void stats_final_kernel(const Partial* __restrict__ parts, int64_t nb, double* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    struct Frame {
+        int64_t lo, hi;
+        int state;
+        Partial left;
+    };
+    Frame st[64];
+    int sp = 0;
+    st[0] = Frame{0, nb, 0, Partial{}};
+    Partial ret{};
+    for (;;) {
+        Frame& f = st[sp];
+        if (f.hi - f.lo == 1) {
+            ret = parts[f.lo];
+            if (sp == 0) break;
+            --sp;
+            continue;
+        }
+        const int64_t size = f.hi - f.lo;
+        int64_t half = 1;
+        while (half * 2 < size) half *= 2;  // largest power of two strictly below size
+        const int64_t mid = f.lo + half;
+        if (f.state == 0) {
+            f.state = 1;
+            st[++sp] = Frame{f.lo, mid, 0, Partial{}};
+        } else if (f.state == 1) {
+            f.left = ret;
+            f.state = 2;
+            st[++sp] = Frame{mid, f.hi, 0, Partial{}};
+        } else {  // combine(x, y) = (min, max, x.sum + y.sum)  (kernels.py:362-363)
+            ret = Partial{fmin(f.left.mn, ret.mn), fmax(f.left.mx, ret.mx), f.left.sum + ret.sum};
+            if (sp == 0) break;
+            --sp;
+        }
     }
-    if (threadIdx.x == 0) {
-        out[0] = sh[0].mn;
-        out[1] = sh[0].mx;
-        out[2] = sh[0].sum;
-    }
+    out[0] = ret.mn;
+    out[1] = ret.mx;
+    out[2] = ret.sum;
 }
 
 // Bin b covers [lo + b w, lo + (b+1) w), the last bin closed above; out-of-range
@@ -104,11 +224,18 @@ __global__ void __launch_bounds__(kThreads) histogram_kernel(const void* __restr
 
 cudaError_t launch_stats(const void* data, int64_t n, int dtype, void* parts, double* out, cudaStream_t st) {
     const int64_t nb = (n + kStatsBlock - 1) / kStatsBlock;
-    if (dtype)
-        stats_blocks_kernel<double><<<(unsigned)nb, kThreads, 0, st>>>(data, n, static_cast<Partial*>(parts));
-    else
-        stats_blocks_kernel<float><<<(unsigned)nb, kThreads, 0, st>>>(data, n, static_cast<Partial*>(parts));
-    stats_final_kernel<<<1, kThreads, 0, st>>>(static_cast<const Partial*>(parts), nb, out);
+    const int rows = kStatsBlock / kLeaf * kLeafPad;
+    if (dtype) {
+        const size_t smem = (size_t)rows * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(stats_blocks_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        stats_blocks_kernel<double><<<(unsigned)nb, kThreads, smem, st>>>(data, n, static_cast<Partial*>(parts));
+    } else {
+        const size_t smem = (size_t)rows * sizeof(float);
+        stats_blocks_kernel<float><<<(unsigned)nb, kThreads, smem, st>>>(data, n, static_cast<Partial*>(parts));
+    }
+    stats_final_kernel<<<1, 32, 0, st>>>(static_cast<const Partial*>(parts), nb, out);
     return cudaGetLastError();
 }
 

@@ -119,6 +119,7 @@ struct Ctx {
     cudaEvent_t band_ev[16] = {};
     cudaEvent_t join_ev = nullptr;
     DevBuf out_scratch;     // device image when the caller passes host memory
+    DevBuf stage_in, stats_parts, stats_res, hist_counts;  // image_stats / image_histogram scratch
     DevBuf fault;           // one u64
     std::string err;
 };
@@ -901,6 +902,10 @@ void nbx_ctx_destroy(void* ctxp) {
     for (auto e : ctx->band_ev)
         if (e) cudaEventDestroy(e);
     ctx->out_scratch.release();
+    ctx->stage_in.release();
+    ctx->stats_parts.release();
+    ctx->stats_res.release();
+    ctx->hist_counts.release();
     ctx->fault.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1024,7 +1029,9 @@ int nbx_image_stats(void* ctxp, const void* data, int64_t n, int dtype, int on_d
         Ctx* ctx = static_cast<Ctx*>(ctxp);
         NBX_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
-        DevBuf in, parts, res;
+        DevBuf& in = ctx->stage_in;
+        DevBuf& parts = ctx->stats_parts;
+        DevBuf& res = ctx->stats_res;
         const void* d = stage_input(ctx, in, data, (size_t)n * (dtype ? 8 : 4), on_device, s);
         parts.ensure(nbx::stats_scratch_bytes(n));
         res.ensure(3 * sizeof(double));
@@ -1051,7 +1058,8 @@ int nbx_image_histogram(void* ctxp, const void* data, int64_t n, int dtype, int 
         Ctx* ctx = static_cast<Ctx*>(ctxp);
         NBX_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
-        DevBuf in, cnt;
+        DevBuf& in = ctx->stage_in;
+        DevBuf& cnt = ctx->hist_counts;
         const void* d = stage_input(ctx, in, data, (size_t)n * (dtype ? 8 : 4), on_device, s);
         cnt.ensure(sizeof(unsigned long long) * ((size_t)n_bins + 2));
         NBX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * ((size_t)n_bins + 2), s));

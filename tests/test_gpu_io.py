@@ -1,6 +1,7 @@
 """GPU: pipelined campaign (F3) against the staged path + reference file format, and device stats (F4)."""
 import json
 import zlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -9,6 +10,8 @@ from paper_2205_07976_b200 import BackgroundProfile, PixelBuffer, simulate_image
 from paper_2205_07976_b200 import io as nio
 
 pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
 
 WATER = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.162, 8.0), (0.3, 6.5)))
 
@@ -41,6 +44,47 @@ def test_write_image_matches_reference_format(gpu, tmp_path):
                          "wavelengths_angstrom", "seed", "image_index", "crc32"}
     data, _ = nio.read_image(p)
     assert np.array_equal(data.reshape(-1), acc.data.astype("<f4"))
+
+
+def reference_stats_total(values: np.ndarray) -> float:
+    """The reference's image_stats total restated with NumPy (kernels.py:346-371): per 8192
+    block float(np.sum(chunk, dtype=np.float64)), then parallel_reduce's tree that splits a
+    span at the largest power of two strictly below its size (execution.py:227-260)."""
+    blocks = [float(np.sum(values[i:i + 8192], dtype=np.float64)) for i in range(0, values.size, 8192)]
+
+    def span(lo, hi):
+        if hi - lo == 1:
+            return blocks[lo]
+        mid = lo + (1 << ((hi - lo - 1).bit_length() - 1))
+        return span(lo, mid) + span(mid, hi)
+
+    return span(0, len(blocks))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [15, 8192, 3 * 8192, 1_000_000, 14_745_600])
+def test_image_stats_total_is_bitwise_the_reference(gpu, dtype, n):
+    """Device image_stats reproduces the reference's FP64 total bit for bit: NumPy's pairwise
+    sum inside each block and the fixed block tree (nbx_reduce.cu), on data whose summation
+    order matters (lognormal over ~14 decades)."""
+    rng = np.random.default_rng(n)
+    vals = np.exp(rng.normal(0.0, 8.0, n)).astype(dtype)
+    st = nio.image_stats(PixelBuffer((1, n), "f32" if dtype == np.float32 else "f64", vals))
+    want = reference_stats_total(vals)
+    assert st.total == want, (st.total, want)
+    assert st.mean == want / n
+    assert st.min == float(vals.min()) and st.max == float(vals.max())
+
+
+def test_image_stats_matches_reference_fixture(gpu):
+    """Against xtrace's own image_stats outputs (tests/golden/stats.npz): every field bitwise."""
+    z = np.load(GOLDEN / "stats.npz")
+    for n, prec, ref in zip(z["n"], z["precision"], z["ref_stats"]):
+        n, prec = int(n), str(prec)
+        rng = np.random.default_rng(n)  # tools/make_golden.py:stats_values
+        v = np.exp(rng.normal(0.0, 8.0, n)).astype(np.float32 if prec == "f32" else np.float64)
+        st = nio.image_stats(PixelBuffer((1, n), prec, v))
+        assert tuple(st) == tuple(float(x) for x in ref), (n, prec, tuple(st), ref)
 
 
 def test_image_stats_and_histogram(gpu):

@@ -117,3 +117,33 @@ def test_oracle_pipeline_matches_reference_fixture():
     bg, _ = oracle.background(_bg_descriptor(*parity.bg_inputs(case)), "f32")
     acc = spots.astype(np.float64) + bg.astype(np.float64)
     np.testing.assert_allclose(acc, case["ref_image"], rtol=1e-7, atol=0)
+
+
+def _stats_values(n, precision):
+    rng = np.random.default_rng(n)  # tools/make_golden.py:stats_values
+    return np.exp(rng.normal(0.0, 8.0, n)).astype(np.float32 if precision == "f32" else np.float64)
+
+
+def reference_stats_total(values):
+    """The reference image_stats total restated with NumPy (kernels.py:346-371, execution.py:227-260)."""
+    blocks = [float(np.sum(values[i:i + 8192], dtype=np.float64)) for i in range(0, values.size, 8192)]
+
+    def span(lo, hi):
+        if hi - lo == 1:
+            return blocks[lo]
+        mid = lo + (1 << ((hi - lo - 1).bit_length() - 1))
+        return span(lo, mid) + span(mid, hi)
+
+    return span(0, len(blocks))
+
+
+def test_stats_restatement_is_the_reference():
+    """tests/golden/stats.npz holds xtrace.kernels.image_stats outputs (run by tools/make_golden.py);
+    the NumPy restatement the GPU test compares against reproduces them bit for bit."""
+    z = np.load(parity.GOLDEN / "stats.npz")
+    for n, prec, ref in zip(z["n"], z["precision"], z["ref_stats"]):
+        v = _stats_values(int(n), str(prec))
+        total = reference_stats_total(v)
+        assert total == ref[3]
+        assert total / n == ref[2]
+        assert float(v.min()) == ref[0] and float(v.max()) == ref[1]

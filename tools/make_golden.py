@@ -205,6 +205,26 @@ def pipeline_case():
     return case, acc.data.copy()
 
 
+STATS_SPECS = [(15, "f32"), (8192, "f64"), (3 * 8192 + 5, "f32"), (1_000_000, "f32"), (1_000_000, "f64")]
+
+
+def stats_values(n: int, precision: str) -> np.ndarray:
+    """Lognormal over ~14 decades (summation order matters), seeded by n."""
+    rng = np.random.default_rng(n)
+    return np.exp(rng.normal(0.0, 8.0, n)).astype(np.float32 if precision == "f32" else np.float64)
+
+
+def stats_case():
+    """xtrace.kernels.image_stats (kernels.py:346-371) on seeded arrays: the reference's bits."""
+    rows = []
+    for n, prec in STATS_SPECS:
+        v = stats_values(n, prec)
+        st = xk.image_stats(xk.PixelBuffer((1, n), prec, v))
+        rows.append([st.min, st.max, st.mean, st.total])
+    return {"n": np.array([n for n, _ in STATS_SPECS]), "precision": np.array([p for _, p in STATS_SPECS]),
+            "ref_stats": np.array(rows)}
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
@@ -234,6 +254,11 @@ def main(names):
         np.savez_compressed(OUT / "pipeline_full.npz", ref_image=acc, **{k: np.asarray(v) for k, v in case.items()})
         meta["pipeline_full"] = {"pixels": int(acc.size), "total": float(acc.sum())}
         print("pipeline_full", meta["pipeline_full"], flush=True)
+    if not names or "stats" in names:
+        case = stats_case()
+        np.savez_compressed(OUT / "stats.npz", **case)
+        meta["stats"] = {"arrays": len(STATS_SPECS), "generator": "tools/make_golden.py:stats_values"}
+        print("stats", case["ref_stats"].tolist(), flush=True)
     old = json.loads((OUT / "index.json").read_text()) if (OUT / "index.json").exists() else {}
     old.update(meta)
     (OUT / "index.json").write_text(json.dumps(old, indent=1, sort_keys=True) + "\n")
