@@ -145,46 +145,52 @@ __global__ void __launch_bounds__(kThreads) stats_blocks_kernel(const void* __re
 }
 
 // parallel_reduce's tree over the block partials (execution.py:227-285): a span splits
-// at the largest power of two strictly below its size; one thread, iteratively.
-__global__ void stats_final_kernel(const Partial* __restrict__ parts, int64_t nb, double* __restrict__ out) {
-    if (threadIdx.x != 0) return;
-    struct Frame {
-        int64_t lo, hi;
-        int state;
-        Partial left;
-    };
-    Frame st[64];
-    int sp = 0;
-    st[0] = Frame{0, nb, 0, Partial{}};
-    Partial ret{};
-    for (;;) {
-        Frame& f = st[sp];
-        if (f.hi - f.lo == 1) {
-            ret = parts[f.lo];
-            if (sp == 0) break;
-            --sp;
-            continue;
+// at the largest power of two strictly below its size.  For nb partials that is the
+// binary decomposition of nb into power-of-two segments [s_k, s_k + 2^e_k) (most
+// significant first), each reduced as a perfect pairwise tree, then combined right to
+// left: T_0 + (T_1 + (... + T_last)).  One block: all segments' tree levels run in
+// parallel in place (global scratch, __syncthreads between levels), then thread 0
+// folds the chain.
+__device__ __forceinline__ Partial combine_p(const Partial& x, const Partial& y) {  // kernels.py:362-363
+    return Partial{fmin(x.mn, y.mn), fmax(x.mx, y.mx), x.sum + y.sum};
+}
+
+__global__ void __launch_bounds__(1024) stats_final_kernel(Partial* __restrict__ parts, int64_t nb,
+                                                           double* __restrict__ out) {
+    int top = 0;
+    while ((int64_t(1) << (top + 1)) <= nb) ++top;  // highest set bit of nb
+    for (int l = 0; l < top; ++l) {
+        const int64_t stride = int64_t(1) << l;
+        // pair (i, i + stride) for i a multiple of 2 stride inside any segment longer than 2 stride
+        for (int64_t q = threadIdx.x; q < nb / (2 * stride); q += blockDim.x) {
+            const int64_t i = q * 2 * stride;
+            // segment of i: the prefix of nb's set bits (most significant first) that contains i
+            int64_t start = 0;
+            int e = top;
+            for (; e >= 0; --e) {
+                if (!((nb >> e) & 1)) continue;
+                if (i < start + (int64_t(1) << e)) break;
+                start += int64_t(1) << e;
+            }
+            if (e > l) parts[i] = combine_p(parts[i], parts[i + stride]);
         }
-        const int64_t size = f.hi - f.lo;
-        int64_t half = 1;
-        while (half * 2 < size) half *= 2;  // largest power of two strictly below size
-        const int64_t mid = f.lo + half;
-        if (f.state == 0) {
-            f.state = 1;
-            st[++sp] = Frame{f.lo, mid, 0, Partial{}};
-        } else if (f.state == 1) {
-            f.left = ret;
-            f.state = 2;
-            st[++sp] = Frame{mid, f.hi, 0, Partial{}};
-        } else {  // combine(x, y) = (min, max, x.sum + y.sum)  (kernels.py:362-363)
-            ret = Partial{fmin(f.left.mn, ret.mn), fmax(f.left.mx, ret.mx), f.left.sum + ret.sum};
-            if (sp == 0) break;
-            --sp;
-        }
+        __syncthreads();
     }
-    out[0] = ret.mn;
-    out[1] = ret.mx;
-    out[2] = ret.sum;
+    if (threadIdx.x != 0) return;
+    // segment roots, least significant (rightmost) first: acc = T_k + acc
+    int64_t end = nb;
+    Partial acc{};
+    bool first = true;
+    for (int e = 0; e <= top; ++e) {
+        if (!((nb >> e) & 1)) continue;
+        const int64_t start = end - (int64_t(1) << e);
+        acc = first ? parts[start] : combine_p(parts[start], acc);
+        first = false;
+        end = start;
+    }
+    out[0] = acc.mn;
+    out[1] = acc.mx;
+    out[2] = acc.sum;
 }
 
 // Bin b covers [lo + b w, lo + (b+1) w), the last bin closed above; out-of-range
@@ -235,7 +241,7 @@ cudaError_t launch_stats(const void* data, int64_t n, int dtype, void* parts, do
         const size_t smem = (size_t)rows * sizeof(float);
         stats_blocks_kernel<float><<<(unsigned)nb, kThreads, smem, st>>>(data, n, static_cast<Partial*>(parts));
     }
-    stats_final_kernel<<<1, 32, 0, st>>>(static_cast<const Partial*>(parts), nb, out);
+    stats_final_kernel<<<1, 1024, 0, st>>>(static_cast<Partial*>(parts), nb, out);
     return cudaGetLastError();
 }
 
