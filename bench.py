@@ -423,6 +423,25 @@ def stage_timings(cx, N, torch, stream, ctx, panel) -> dict:
         if nbytes:
             row.update({"algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak})
         res[name] = row
+    # F3: the pipelined campaign (fused spots+background per image, .bin + sidecar with CRC-32,
+    # download/CRC/write of image i overlapped with image i+1's kernel), 4 images after one warm-up
+    import shutil
+    import tempfile
+
+    from paper_2205_07976_b200.io import run_campaign
+    from paper_2205_07976_b200 import synthetic
+
+    out_dir = Path(tempfile.mkdtemp(prefix="nbx_bench_campaign_"))
+    try:
+        def cfor(i):
+            return synthetic.ls49_context(synthetic.SEED + 5000 + i, panel=panel, compute=ctx.compute)
+
+        run_campaign(cfor, 1, out_dir, background=water)
+        r = run_campaign(cfor, 4, out_dir, first_image=1, background=water)
+        res["campaign"] = {"images": 4, "ms_per_image": 1e3 * r.seconds / 4, "images_per_s": 4 / r.seconds,
+                           "basis": "host wall time of io.run_campaign (nbx_campaign) incl. file writes"}
+    finally:
+        shutil.rmtree(out_dir, ignore_errors=True)
     return res
 
 

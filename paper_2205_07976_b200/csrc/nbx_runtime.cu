@@ -108,6 +108,7 @@ struct Ctx {
     Plan* camp_plan[2] = {nullptr, nullptr};
     DevBuf camp_out[2], camp_fault[2];
     void* camp_host[2] = {nullptr, nullptr};
+    unsigned long long* camp_fault_host = nullptr;  // pinned [2][kFaultSlots]
     size_t camp_host_bytes = 0;
     Plan* oneshot = nullptr;  // device buffers reused by nbx_spots (cudaFree can stall for ~100 ms)
     cudaStream_t own = nullptr;
@@ -896,6 +897,7 @@ void nbx_ctx_destroy(void* ctxp) {
         ctx->camp_fault[b].release();
         if (ctx->camp_host[b]) cudaFreeHost(ctx->camp_host[b]);
     }
+    if (ctx->camp_fault_host) cudaFreeHost(ctx->camp_fault_host);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
     if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
@@ -1105,7 +1107,13 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
         };
         cudaEvent_t all[4] = {kdone[0], kdone[1], copied[0], copied[1]};
         Events guard{all};
-        unsigned long long hfault[2][kFaultSlots];
+        // fault slots come back through PINNED memory: a cudaMemcpyAsync into pageable memory
+        // would block the host until the copy stream reached it (i.e. until the NEXT image's
+        // kernel finished), serialising the write-out with the GPU
+        if (!ctx->camp_fault_host)
+            NBX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->camp_fault_host),
+                                   2 * kFaultSlots * sizeof(unsigned long long), cudaHostAllocDefault));
+        unsigned long long* hfault[2] = {ctx->camp_fault_host, ctx->camp_fault_host + kFaultSlots};
         size_t bytes[2] = {0, 0};
         // render image i into slot i % 2: plan build (host), launch, then async D2H + fault read
         auto launch = [&](int i) {
@@ -1117,7 +1125,8 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                          static_cast<unsigned long long*>(ctx->camp_fault[b].p), cs);
             NBX_CUDA(cudaEventRecord(kdone[b], cs));
             NBX_CUDA(cudaStreamWaitEvent(ds, kdone[b], 0));
-            NBX_CUDA(cudaMemcpyAsync(hfault[b], ctx->camp_fault[b].p, sizeof(hfault[b]), cudaMemcpyDeviceToHost, ds));
+            NBX_CUDA(cudaMemcpyAsync(hfault[b], ctx->camp_fault[b].p, kFaultSlots * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, ds));
             NBX_CUDA(cudaMemcpyAsync(ctx->camp_host[b], ctx->camp_out[b].p, bytes[b], cudaMemcpyDeviceToHost, ds));
             NBX_CUDA(cudaEventRecord(copied[b], ds));
         };
@@ -1145,12 +1154,19 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                 NBX_CUDA(cudaStreamSynchronize(ds));
                 return NBX_OK;
             }
+            const auto t0 = std::chrono::steady_clock::now();
             crcs[i] = crc32_update(0, static_cast<const unsigned char*>(ctx->camp_host[b]), bytes[b]);
+            const auto t1 = std::chrono::steady_clock::now();
             FILE* fh = std::fopen(paths[i], "wb");
             if (!fh) throw ArgError(std::string("cannot open ") + paths[i]);
             const size_t wrote = std::fwrite(ctx->camp_host[b], 1, bytes[b], fh);
             const int closed = std::fclose(fh);
             if (wrote != bytes[b] || closed != 0) throw ArgError(std::string("short write to ") + paths[i]);
+            if (trace_enabled()) {
+                const auto t2 = std::chrono::steady_clock::now();
+                auto ms = [](auto a, auto c) { return std::chrono::duration<double, std::milli>(c - a).count(); };
+                std::fprintf(stderr, "[nbx] campaign image %d: crc %.2f ms, write %.2f ms\n", i, ms(t0, t1), ms(t1, t2));
+            }
         }
         return NBX_OK;
     });
