@@ -145,6 +145,11 @@ def run_ours(args):
     if args.mode == "jungfrau" and args.compute == "fp32" and "--compute" not in sys.argv:
         args.compute = "fp64"
     world, rank, local = dist_env()
+    # NBX_BENCH_SHARE_GPU=1 (test only): every rank on cuda:0 with gloo collectives, to exercise
+    # the multi-rank control flow on a one-GPU box; real runs are one rank per GPU over NCCL
+    share = os.environ.get("NBX_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     os.environ["NBX_DEVICE"] = str(local)
     import numpy as np
     import torch
@@ -152,7 +157,10 @@ def run_ours(args):
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from oracle import oracle  # cpu_baseline leg only (the checker, never the thing measured)
     from paper_2205_07976_b200 import PixelBuffer, SpotsPlan, nanobragg_spots, synthetic
