@@ -171,14 +171,16 @@ int nbx_spots(void* ctx, const nbx_spots_desc* d, int compute, int out_mode,
  * NBX_OUT_IMAGE_F32, i.e. write_image's refusal, io.py:409-411). */
 int nbx_fault_stage(void* ctx);
 
-/* Batch of independent images (SURVEY §8 E1 image sharding, config C3):
- * outs[i] receives image i; images share nothing and launch back to back
- * with device-to-host copies overlapped on a second stream. */
+/* Batch of independent images (SURVEY §8 E1 image sharding, config C3; the per-rank
+ * image loop of run_campaign, scheduler.py:190-247): outs[i] receives image i; images
+ * share nothing.  Each image is one nbx_spots call, so a host `out` is downloaded in row
+ * bands overlapping that image's own computation. */
 int nbx_spots_batch(void* ctx, const nbx_spots_desc* descs, int n_images, int compute,
                     int out_mode, void* const* outs, int out_on_device, int64_t* first_bad);
 
 /* Plan API: upload a descriptor once (tables, bases, channels resident in
- * HBM), then run it any number of times. */
+ * HBM), then run it any number of times -- the device analogue of the reference's
+ * per-panel geometry cache (_panel_geometry's lru_cache, kernels.py:158). */
 void* nbx_plan_create(void* ctx, const nbx_spots_desc* d, int compute);
 int nbx_plan_run(void* plan, int out_mode, void* out, int out_on_device, int64_t* first_bad);
 int nbx_plan_info(void* plan, nbx_plan_info_t* info);
@@ -195,8 +197,10 @@ void nbx_plan_destroy(void* plan);
 int nbx_campaign(void* ctx, const nbx_spots_desc* descs, int n_images, int compute,
                  const char* const* paths, uint32_t* crcs, int64_t* first_bad);
 
-/* Image statistics over n values (dtype 0 f32, 1 f64): out = {min, max, mean, total},
- * deterministic fixed-tree sum (image_stats, kernels.py:346-371).  n >= 1. */
+/* Image statistics over n values (dtype 0 f32, 1 f64): out = {min, max, mean, total}
+ * (image_stats, kernels.py:346-371), the total bit for bit the reference's: NumPy's
+ * pairwise sum inside each 8192-value block, parallel_reduce's power-of-two tree across
+ * blocks (execution.py:227-285).  n >= 1. */
 int nbx_image_stats(void* ctx, const void* data, int64_t n, int dtype, int on_device, double* out4);
 
 /* Histogram (image_histogram, kernels.py:386-430): counts[n_bins] for [lo, hi] with the top
