@@ -504,14 +504,23 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             // chunk is padded with a zero-weight copy of its last channel
             std::vector<nbx::ChunkF32> chunks;
             std::vector<float> ch;
+            // Chunks hold <= kChunkMax channels (the FP32 partial of each packed half sums
+            // <= 64 terms) and a phase-feasible run of L channels is cut into ceil(L / max)
+            // chunks of equal size (C2's 100 channels: one chunk; 130: 66 + 64, not 128 + 2).
             int i0 = 0, npairs = 0;
             const char* cev = std::getenv("NBX_CHUNK_MAX");
-            const int chunk_max = cev ? std::max(2, std::atoi(cev)) : 64;
+            const int chunk_max = cev ? std::max(2, std::atoi(cev)) : 128;
             const char* pev = std::getenv("NBX_PAD_PAIRS");
             const int pad_pairs = pev ? std::max(1, std::atoi(pev)) : 1;
+            int run_end = 0, run_chunk = chunk_max;
             while (i0 < n_src) {
-                int i1 = i0 + 1;
-                while (i1 < n_src && i1 - i0 < chunk_max && (iv[order[i1]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++i1;
+                if (i0 >= run_end) {  // next phase-feasible run and its balanced chunk size
+                    run_end = i0 + 1;
+                    while (run_end < n_src && (iv[order[run_end]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++run_end;
+                    const int len = run_end - i0, k = (len + chunk_max - 1) / chunk_max;
+                    run_chunk = std::min(chunk_max, ((len + k - 1) / k + 1) / 2 * 2);  // even: whole pairs
+                }
+                const int i1 = std::min(run_end, i0 + run_chunk);
                 const double iv0 = 0.5 * (iv[order[i0]] + iv[order[i1 - 1]]);
                 const int p0 = npairs;
                 for (int q = i0; q < i1; q += 2) {
