@@ -141,6 +141,19 @@ struct Plan {
     nbx::SpotsParams P{};
     DevBuf panels, bases, chan, chunks, table, runs;
     HostBuf host_table;       // pinned staging of the F^2 grid
+    // The device F^2 grid is rebuilt only when its inputs change: consecutive images of one
+    // crystal (new orientation / mosaic / spectrum jitter) share the table, so a re-used plan
+    // (nbx_spots' one-shot plan, the campaign's two) skips the fill, validation and upload.
+    struct TableKey {
+        bool valid = false;
+        int compute = -1;
+        int hmax[3] = {0, 0, 0};
+        int32_t sH = 0, sK = 0;
+        double default_f = 0.0, sigma = 0.0, maxf2 = 0.0;
+        const void* dev = nullptr;
+        std::vector<int32_t> hkl;
+        std::vector<double> amp;
+    } tkey;
     BgBufs bg;
     bool uniform_panels = true;  // every panel has the same (slow, fast): row bands are 2-D copies
     int64_t n_pixels = 0;
@@ -220,15 +233,18 @@ void validate(const nbx_spots_desc* d) {
     if (d->shape < 0 || d->shape > 3) throw ArgError("unknown shape transform");
     if (d->n_entries < 0 || (d->n_entries > 0 && (!d->hkl || !d->amplitudes)))
         throw ArgError("structure-factor table arrays missing");
+    if (!finite(d->default_f) || d->default_f < 0) throw ArgError("default_f must be finite and non-negative");
+    const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
+    if (sb < 0 || se > d->n_sources || sb >= se) throw ArgError("invalid source shard range");
+}
+
+void validate_entries(const nbx_spots_desc* d) {
     for (int i = 0; i < d->n_entries; ++i) {
         const double f = d->amplitudes[i];
         if (!finite(f) || f < 0) throw ArgError("amplitudes must be finite and >= 0");
         for (int a = 0; a < 3; ++a)
             if (std::abs((int64_t)d->hkl[3 * i + a]) >= (1 << 20)) throw ArgError("Miller index out of supported range");
     }
-    if (!finite(d->default_f) || d->default_f < 0) throw ArgError("default_f must be finite and non-negative");
-    const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
-    if (sb < 0 || se > d->n_sources || sb >= se) throw ArgError("invalid source shard range");
 }
 
 // Largest |s_out - beam| over every sub-pixel / layer position of every panel.
@@ -347,8 +363,28 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
 }
 
 // Build (or, with `reuse`, rebuild in place -- its device buffers only grow) a plan.
+// NBX_TRACE: wall time of the phases of a plan build, printed to stderr.
+struct PhaseTimer {
+    bool on = trace_enabled();
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    std::string log;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        char buf[64];
+        std::snprintf(buf, sizeof(buf), " %s %.3f", what, std::chrono::duration<double, std::milli>(n - t).count());
+        log += buf;
+        t = n;
+    }
+    ~PhaseTimer() {
+        if (on && !log.empty()) std::fprintf(stderr, "[nbx] plan ms:%s\n", log.c_str());
+    }
+};
+
 Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = nullptr) {
+    PhaseTimer pt;
     validate(d);
+    pt.mark("validate");
     if (compute != NBX_COMPUTE_FP64 && compute != NBX_COMPUTE_FP32) throw ArgError("unknown compute path");
     auto plan = reuse ? reuse : new Plan();
     if (reuse) {
@@ -451,6 +487,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         for (int dd = 0; dd < d->n_domains; ++dd)
             for (int a = 0; a < 3; ++a) smax = std::max(smax, norm3(d->bases + 9 * dd + 3 * a) * relmax);
 
+        pt.mark("geometry");
         // F^2 grid (FP64 exact; FP32 scaled by a power of two sigma), built straight
         // into pinned staging memory: first the largest reachable F^2, then the fill
         const double def2 = d->default_f * d->default_f;
@@ -462,9 +499,22 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             return (int64_t)(d->hkl[3 * i] + hmax[0]) * P.sH + (int64_t)(d->hkl[3 * i + 1] + hmax[1]) * P.sK +
                    (d->hkl[3 * i + 2] + hmax[2]);
         };
+        Plan::TableKey& tk = plan->tkey;
+        const bool same_entries =
+            tk.valid && tk.compute == compute && tk.default_f == d->default_f && tk.sH == P.sH && tk.sK == P.sK &&
+            tk.hmax[0] == hmax[0] && tk.hmax[1] == hmax[1] && tk.hmax[2] == hmax[2] &&
+            tk.hkl.size() == 3 * (size_t)d->n_entries && tk.amp.size() == (size_t)d->n_entries &&
+            (d->n_entries == 0 ||
+             (std::memcmp(tk.hkl.data(), d->hkl, tk.hkl.size() * sizeof(int32_t)) == 0 &&
+              std::memcmp(tk.amp.data(), d->amplitudes, tk.amp.size() * sizeof(double)) == 0));
         double maxf2 = def2;
-        for (int i = 0; i < d->n_entries; ++i)
-            if (reachable(i)) maxf2 = std::max(maxf2, d->amplitudes[i] * d->amplitudes[i]);
+        if (same_entries) {
+            maxf2 = tk.maxf2;
+        } else {
+            validate_entries(d);
+            for (int i = 0; i < d->n_entries; ++i)
+                if (reachable(i)) maxf2 = std::max(maxf2, d->amplitudes[i] * d->amplitudes[i]);
+        }
         double sigma = 1.0;
         if (compute == NBX_COMPUTE_FP32) {
             double maxw = 0.0;
@@ -476,6 +526,15 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 e = std::max(-1000, std::min(e, 100));
                 sigma = std::ldexp(1.0, e);
             }
+        }
+        // device table still current: same entries, grid and scale, buffer not reallocated
+        const size_t tbytes = (size_t)cells_alloc * (compute == NBX_COMPUTE_FP32 ? sizeof(float) : sizeof(double));
+        const bool table_current = same_entries && tk.sigma == sigma && tk.dev == plan->table.p &&
+                                   plan->table.bytes >= tbytes;
+        if (!table_current) tk.valid = false;  // re-armed after the upload below
+        if (table_current) {
+            // nothing to fill or upload
+        } else if (compute == NBX_COMPUTE_FP32) {
             float* tf = plan->host_table.ensure<float>(cells_alloc);
             std::fill(tf, tf + cells_alloc, (float)(def2 * sigma));
             for (int i = 0; i < d->n_entries; ++i)
@@ -487,6 +546,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 if (reachable(i)) t64[cell_of(i)] = d->amplitudes[i] * d->amplitudes[i];
         }
         plan->out_scale = plan->scale / sigma;
+        pt.mark("grid");
 
         // channels
         int n_chan_entries = n_src;  // FP64: channels; FP32: channel pairs
@@ -548,9 +608,11 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                                 cudaMemcpyHostToDevice));
             P.chunks = static_cast<const nbx::ChunkF32*>(plan->chunks.p);
             P.n_chunks = (int32_t)chunks.size();
-            plan->table.ensure(cells_alloc * sizeof(float));
-            NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells_alloc * sizeof(float),
-                                cudaMemcpyHostToDevice));
+            if (!table_current) {
+                plan->table.ensure(cells_alloc * sizeof(float));
+                NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells_alloc * sizeof(float),
+                                    cudaMemcpyHostToDevice));
+            }
         } else {
             // Channel-recurrence variant (sincg): channels sorted by 1/lambda and cut into
             // runs whose 1/lambda are an arithmetic progression to within 1e-14 of phase
@@ -603,9 +665,26 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 P.runs = static_cast<const nbx::RunF64*>(plan->runs.p);
                 P.n_runs = (int32_t)runs.size();
             }
-            plan->table.ensure(cells * sizeof(double));
-            NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells * sizeof(double), cudaMemcpyHostToDevice));
+            if (!table_current) {
+                plan->table.ensure(cells * sizeof(double));
+                NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells * sizeof(double),
+                                    cudaMemcpyHostToDevice));
+            }
         }
+        if (!table_current) {
+            tk.compute = compute;
+            tk.default_f = d->default_f;
+            tk.sH = P.sH;
+            tk.sK = P.sK;
+            for (int a = 0; a < 3; ++a) tk.hmax[a] = hmax[a];
+            tk.sigma = sigma;
+            tk.maxf2 = maxf2;
+            tk.dev = plan->table.p;
+            tk.hkl.assign(d->hkl, d->hkl + 3 * (size_t)d->n_entries);
+            tk.amp.assign(d->amplitudes, d->amplitudes + d->n_entries);
+            tk.valid = true;
+        }
+        pt.mark("channels+upload");
         if ((size_t)n_src * 16 > 200 * 1024) throw ArgError("too many sources in one shard (max 12800)");
 
         plan->bases.ensure(sizeof(double) * 9 * d->n_domains);
@@ -636,6 +715,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         P.out_scale = plan->out_scale;
         setup_background(d, P, plan->bg);
 
+        pt.mark("rest");
         nbx_plan_info_t& I = plan->info;
         I.n_pixels = plan->n_pixels;
         I.steps = plan->steps;

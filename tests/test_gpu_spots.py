@@ -370,6 +370,32 @@ def test_pipelined_host_download_is_bitwise_the_device_image(gpu, layout, comput
     plan.close()
 
 
+@pytest.mark.parametrize("compute", ["fp32", "fp64"])
+def test_reused_plan_tracks_table_changes(gpu, compute):
+    """nanobragg_spots re-uses one plan and keeps the device F^2 grid when the structure-factor
+    table is unchanged (nbx_runtime.cu: TableKey); alternating tables, a changed default_f and
+    a rescaling weight must each give exactly the image of a fresh plan."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import StructureFactorTable, _native as N
+
+    base = roi_ctx(compute, centre=True)
+    t0 = base.crystal.sf_table
+    hkl, amp = t0.arrays()
+    t1 = StructureFactorTable({tuple(int(v) for v in h): 2.0 * float(a) for h, a in zip(hkl, amp)}, t0.default_f)
+    t2 = StructureFactorTable({tuple(int(v) for v in h): float(a) for h, a in zip(hkl, amp)}, t0.default_f + 3.0)
+    spec_big = BeamSpectrum(samples=tuple((float(l), 1e6 * float(w)) for l, w in base.spectrum.samples),
+                            fluence=base.spectrum.fluence, polarization_on=base.spectrum.polarization_on)
+    ctxs = [base, dataclasses.replace(base, crystal=dataclasses.replace(base.crystal, sf_table=t1)), base,
+            dataclasses.replace(base, crystal=dataclasses.replace(base.crystal, sf_table=t2)),
+            dataclasses.replace(base, spectrum=spec_big), base]
+    for ctx in ctxs:
+        got = run(ctx, "f64").data
+        fresh = np.zeros(got.size)
+        SpotsPlan(ctx).run(fresh, mode=N.OUT_F64)
+        assert np.array_equal(got, fresh)
+
+
 def test_add_array_upcast_semantics(gpu):
     lhs = PixelBuffer((1, 3), "f64", [0.0, 1.0, 2.0])
     rhs = PixelBuffer((1, 3), "f32", [0.1, 0.5, 0.25])
