@@ -289,6 +289,9 @@ def run_ours(args):
         "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
                      "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
                      "traffic": traffic,
+                     # the image write-back (the path's only HBM stream; north_star asks for it)
+                     "writeback": {"bytes_per_image": int(plans[0].n_pixels) * 4,
+                                   "gbs": plans[0].n_pixels * 4 / (mean_kernel / 1e3) / 1e9},
                      "basis": f"{STEP_INSTR} FP-pipe instr/step x 2 FLOP x steps / mean spot-kernel time; "
                               "peak = live FMA probe (nbx_probe_fma_peak) on this GPU"},
         "clocks": clocks.summary(),
