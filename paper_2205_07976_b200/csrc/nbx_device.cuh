@@ -219,16 +219,8 @@ __device__ __forceinline__ f2x pk2(float lo, float hi) {
     return r;
 }
 __device__ __forceinline__ f2x bc2(float a) { return pk2(a, a); }
-__device__ __forceinline__ float lo2(f2x v) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-    return a;
-}
-__device__ __forceinline__ float hi2(f2x v) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-    return b;
-}
+__device__ __forceinline__ float lo2(f2x v) { return __uint_as_float((unsigned)(v & 0xFFFFFFFFull)); }
+__device__ __forceinline__ float hi2(f2x v) { return __uint_as_float((unsigned)(v >> 32)); }
 __device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
     f2x d;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));

@@ -570,8 +570,6 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             int i0 = 0, npairs = 0;
             const char* cev = std::getenv("NBX_CHUNK_MAX");
             const int chunk_max = cev ? std::max(2, std::atoi(cev)) : 128;
-            const char* pev = std::getenv("NBX_PAD_PAIRS");
-            const int pad_pairs = pev ? std::max(1, std::atoi(pev)) : 1;
             int run_end = 0, run_chunk = chunk_max;
             while (i0 < n_src) {
                 if (i0 >= run_end) {  // next phase-feasible run and its balanced chunk size
@@ -589,12 +587,6 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                     ch.push_back((float)(iv[order[q1]] - iv0));
                     ch.push_back((float)d->weights[sb + order[q]]);
                     ch.push_back(q + 1 < i1 ? (float)d->weights[sb + order[q1]] : 0.0f);
-                    ++npairs;
-                }
-                while ((npairs - p0) % pad_pairs) {  // zero-weight pairs up to a multiple of the unroll
-                    for (int r = 0; r < 2; ++r) ch.push_back((float)(iv[order[i1 - 1]] - iv0));
-                    ch.push_back(0.0f);
-                    ch.push_back(0.0f);
                     ++npairs;
                 }
                 chunks.push_back(nbx::ChunkF32{iv0, p0, npairs});
