@@ -107,23 +107,61 @@ constexpr double kInvPi6 = 1.0 / 961.38919357530443703021944;  // pi^-6
 // by the index FMA chain is directly the biased cell number.
 // ---------------------------------------------------------------------------
 
+// Fhkl index kinds: 0 dense power-of-two grid indexed by magic-float bit patterns
+// (FP32 packed loop), 1 dense grid indexed by integers, 2 sparse hash (huge cells).
+enum { kIdxMagic = 0, kIdxWide = 1, kIdxHash = 2 };
+
+constexpr unsigned long long kHashEmpty = ~0ull;
+
+__device__ __forceinline__ unsigned long long pack_hkl(int h, int k, int l) {
+    return ((unsigned long long)(uint32_t)(h + (1 << 20)) << 42) | ((unsigned long long)(uint32_t)(k + (1 << 20)) << 21) |
+           (unsigned long long)(uint32_t)(l + (1 << 20));
+}
+
+__device__ __forceinline__ uint32_t hash_slot(unsigned long long key, uint32_t mask) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+
+// F^2 of integer (h, k, l) from the sparse table; linear probing, table at most half full.
+template <typename T>
+__device__ __forceinline__ T hash_f2(const unsigned long long* __restrict__ keys, const T* __restrict__ vals,
+                                     uint32_t mask, T def, int h, int k, int l) {
+    const int lim = 1 << 20;
+    if (h <= -lim || h >= lim || k <= -lim || k >= lim || l <= -lim || l >= lim) return def;
+    const unsigned long long key = pack_hkl(h, k, l);
+    uint32_t s = hash_slot(key, mask);
+    for (;;) {
+        const unsigned long long kk = __ldg(keys + s);
+        if (kk == key) return __ldg(vals + s);
+        if (kk == kHashEmpty) return def;
+        s = (s + 1) & mask;
+    }
+}
+
 // The few launch constants the scalar form needs, passed BY VALUE: a reference
 // to the kernel's parameter block would make the compiler copy all of it into
 // a local-memory stack frame in every thread (256 B of stores per pixel).
 struct ScalarArgs {
     float Na, Nb, Nc, nnn;
     int32_t sH, sK, sh_h, sh_k;
+    const unsigned long long* hkeys;
+    const float* hvals;
+    uint32_t hmask;
+    float hdef;
 };
 
 __device__ __forceinline__ ScalarArgs scalar_args(const SpotsParams& P) {
-    return ScalarArgs{P.n_cells_f[0], P.n_cells_f[1], P.n_cells_f[2], P.nnn_f, P.sH, P.sK, P.sh_h, P.sh_k};
+    return ScalarArgs{P.n_cells_f[0], P.n_cells_f[1], P.n_cells_f[2], P.nnn_f, P.sH, P.sK, P.sh_h, P.sh_k,
+                      P.hash_keys, static_cast<const float*>(P.hash_vals), P.hash_mask, P.hash_def_f};
 }
 
-// Scalar form: the biased re-evaluation, the non-grating shapes, the WIDE index.
-template <int SHAPE, bool WIDE, int PDEG, bool BIAS>
+// Scalar form: the biased re-evaluation, the non-grating shapes, the wide and hash indices.
+// (na0, nb0, nc0) is the chunk anchor's integer part (hash index only).
+template <int SHAPE, int IDX, int PDEG, bool BIAS>
 __device__ __noinline__ float chunk_sum_f32_scalar(const ScalarArgs P, const float4* __restrict__ sch, int p0,
                                                    int p1, float a_hi, float b_hi, float c_hi, float fa, float fb,
-                                                   float fc, float magic_c, const float* __restrict__ base) {
+                                                   float fc, float magic_c, const float* __restrict__ base, int na0,
+                                                   int nb0, int nc0) {
     const float Na = P.Na, Nb = P.Nb, Nc = P.Nc;
     float accf = 0.0f;
     for (int q = 2 * p0; q < 2 * p1; ++q) {
@@ -143,13 +181,16 @@ __device__ __noinline__ float chunk_sum_f32_scalar(const ScalarArgs P, const flo
             L2 = shape_latt2<SHAPE, float>(__fmaf_rn(x, x, __fmaf_rn(y, y, z * z)), P.nnn);
         }
         float F2;
-        if constexpr (!WIDE) {
+        if constexpr (IDX == kIdxMagic) {
             const uint32_t cell = (__float_as_uint(A.m) << P.sh_h) + (__float_as_uint(B.m) << P.sh_k) +
                                   __float_as_uint(C.m);
             F2 = __ldg(base + cell);
-        } else {
+        } else if constexpr (IDX == kIdxWide) {
             const int off = __float2int_rn(A.j) * P.sH + __float2int_rn(B.j) * P.sK + __float2int_rn(C.j);
             F2 = __ldg(base + off);
+        } else {
+            F2 = hash_f2<float>(P.hkeys, P.hvals, P.hmask, P.hdef, na0 + __float2int_rn(A.j),
+                                nb0 + __float2int_rn(B.j), nc0 + __float2int_rn(C.j));
         }
         accf = __fmaf_rn(F2 * wt, L2, accf);
     }
@@ -190,7 +231,7 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
     return lo2(acc) + hi2(acc);
 }
 
-template <int SHAPE, bool WIDE, int PDEG>
+template <int SHAPE, int IDX, int PDEG>
 __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const ChunkF32* __restrict__ sck,
                                                  const float4* __restrict__ sch, double Sa, double Sb,
                                                  double Sc) {
@@ -204,38 +245,53 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
         const float fa = __double2float_rn(ha - (double)na);
         const float fb = __double2float_rn(hb - (double)nb);
         const float fc = __double2float_rn(hc - (double)nc);
-        const int64_t cell0 = (int64_t)(na - P.lo[0]) * P.sH + (int64_t)(nb - P.lo[1]) * P.sK + (nc - P.lo[2]);
-        // !WIDE: the l-axis magic carries cell0 and base absorbs the float bias;
-        // WIDE: per-chunk base + integer offset
-        const float magic_c = WIDE ? kMagicF32 : kMagicF32 + (float)cell0;
-        const float* base = static_cast<const float*>(P.table) + (WIDE ? cell0 : -(int64_t)P.lea_bias);
+        // magic: the l-axis magic carries cell0 and base absorbs the float bias;
+        // wide: per-chunk base + integer offset; hash: absolute indices from the anchor
+        const int64_t cell0 = IDX == kIdxHash ? 0
+                                              : (int64_t)(na - P.lo[0]) * P.sH + (int64_t)(nb - P.lo[1]) * P.sK +
+                                                    (nc - P.lo[2]);
+        const float magic_c = IDX == kIdxMagic ? kMagicF32 + (float)cell0 : kMagicF32;
+        const float* base = IDX == kIdxHash ? nullptr
+                                            : static_cast<const float*>(P.table) +
+                                                  (IDX == kIdxWide ? cell0 : -(int64_t)P.lea_bias);
         float accf;
-        if constexpr (SHAPE == 0 && !WIDE) {
+        if constexpr (SHAPE == 0 && IDX == kIdxMagic) {
             accf = chunk_sum_f32x2<PDEG>(P, sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb, fc, magic_c, base);
         } else {
-            accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, false>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa,
-                                                                  fb, fc, magic_c, base);
+            accf = chunk_sum_f32_scalar<SHAPE, IDX, PDEG, false>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi,
+                                                                 c_hi, fa, fb, fc, magic_c, base, na, nb, nc);
         }
-        if constexpr (SHAPE == 0 && !WIDE && kMufuNum<PDEG>) {
+        if constexpr (SHAPE == 0 && IDX == kIdxMagic && kMufuNum<PDEG>) {
             // MUFU numerators are sin(pi N t), the polynomial denominators sin(pi t)/pi
             if (isfinite(accf))
                 dacc += (double)accf * kInvPi6;
             else  // exact Bragg position / underflow: the reference's limit branch (polynomial form)
-                dacc += (double)chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi,
-                                                                              c_hi, fa, fb, fc, magic_c, base);
+                dacc += (double)chunk_sum_f32_scalar<SHAPE, IDX, PDEG, true>(
+                    scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi, c_hi, fa, fb, fc, magic_c, base, na, nb, nc);
             continue;
         }
         if constexpr (SHAPE == 0) {
             if (!isfinite(accf))  // exact Bragg position / underflow: the reference's limit branch
-                accf = chunk_sum_f32_scalar<SHAPE, WIDE, PDEG, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi, c_hi,
-                                                                     fa, fb, fc, magic_c, base);
+                accf = chunk_sum_f32_scalar<SHAPE, IDX, PDEG, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi, b_hi,
+                                                                    c_hi, fa, fb, fc, magic_c, base, na, nb, nc);
         }
         dacc += (double)accf;
     }
     return dacc;
 }
 
-template <int SHAPE, bool BIAS>
+// F^2 of integer (h, k, l) on the FP64 path: dense grid (index kinds 0/1) or sparse table.
+template <int IDX>
+__device__ __forceinline__ double f2_f64(const SpotsParams& P, const double* __restrict__ tab, int l0, int h, int k,
+                                         int l) {
+    if constexpr (IDX == kIdxHash)
+        return hash_f2<double>(P.hash_keys, static_cast<const double*>(P.hash_vals), P.hash_mask, P.hash_def_d, h, k,
+                               l);
+    else
+        return __ldg(tab + (h * P.sH + k * P.sK + l - l0));
+}
+
+template <int SHAPE, bool BIAS, int IDX>
 __device__ __forceinline__ double channel_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
                                                   double Sa, double Sb, double Sc) {
     const double Na = P.n_cells_d[0], Nb = P.n_cells_d[1], Nc = P.n_cells_d[2];
@@ -259,19 +315,18 @@ __device__ __forceinline__ double channel_sum_f64(const SpotsParams& P, const do
             L2 = shape_latt2<SHAPE, double>(x * x + y * y + z * z, P.nnn_d);
         }
         // integral doubles -> int on the (otherwise idle) conversion unit, index on the ALU
-        const int idx = __double2int_rz(A.n) * P.sH + __double2int_rz(B.n) * P.sK + __double2int_rz(C.n) - l0;
-        const double F2 = __ldg(tab + idx);
+        const double F2 = f2_f64<IDX>(P, tab, l0, __double2int_rz(A.n), __double2int_rz(B.n), __double2int_rz(C.n));
         acc = __fma_rn(F2 * c.y, L2, acc);
     }
     return acc;
 }
 
-template <int SHAPE>
+template <int SHAPE, int IDX>
 __device__ __forceinline__ double domain_sum_f64(const SpotsParams& P, const double2* __restrict__ sch,
                                                  double Sa, double Sb, double Sc) {
-    double acc = channel_sum_f64<SHAPE, false>(P, sch, Sa, Sb, Sc);
+    double acc = channel_sum_f64<SHAPE, false, IDX>(P, sch, Sa, Sb, Sc);
     if constexpr (SHAPE == 0) {
-        if (!isfinite(acc)) acc = channel_sum_f64<SHAPE, true>(P, sch, Sa, Sb, Sc);
+        if (!isfinite(acc)) acc = channel_sum_f64<SHAPE, true, IDX>(P, sch, Sa, Sb, Sc);
     }
     return acc;
 }
@@ -343,6 +398,7 @@ __device__ __forceinline__ AxisRec axis_rec(double S, double iv0, double delta, 
 __device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu; }
 
 // One channel from the three axes' current sines: w F^2 F_latt^2.
+template <int IDX>
 __device__ __forceinline__ double rec_channel(const SpotsParams& P, const double* __restrict__ tab, int l0,
                                               double2 c, double Sa, double Sb, double Sc, double ad, double an,
                                               double bd, double bn, double cd, double cn) {
@@ -361,9 +417,10 @@ __device__ __forceinline__ double rec_channel(const SpotsParams& P, const double
         dd = (a.den * b.den) * e.den;
     }
     const double ratio = nn * rcp_f64<kNewtonF64>(dd);
-    return (__ldg(tab + (ia * P.sH + ib * P.sK + ic - l0)) * c.y) * (ratio * ratio);
+    return (f2_f64<IDX>(P, tab, l0, ia, ib, ic) * c.y) * (ratio * ratio);
 }
 
+template <int IDX>
 __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const double2* __restrict__ sch,
                                                      const RunF64* __restrict__ sru, double Sa, double Sb,
                                                      double Sc) {
@@ -377,7 +434,7 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
         AxisRec C = axis_rec(Sc, run.iv0, run.delta, P.n_cells_d[2]);
 #pragma unroll kRecUnroll
         for (int w = run.begin; w < run.end; ++w) {
-            acc += rec_channel(P, tab, l0, sch[w], Sa, Sb, Sc, A.den.s, A.num.s, B.den.s, B.num.s, C.den.s,
+            acc += rec_channel<IDX>(P, tab, l0, sch[w], Sa, Sb, Sc, A.den.s, A.num.s, B.den.s, B.num.s, C.den.s,
                                C.num.s);
             advance(A.den);
             advance(A.num);
@@ -394,7 +451,7 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
 // The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path, 2 = FP64 path with
 // the channel recurrence (sincg only).
 // ---------------------------------------------------------------------------
-template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
+template <int COMPUTE, int SHAPE, int IDX, int PDEG>
 __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : NBX_MIN_BLOCKS_F64) spots_kernel(const SpotsParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.y * kBlockX + threadIdx.x;
@@ -465,17 +522,17 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
                     const double Sb = r0 * __ldg(B + 3) + r1 * __ldg(B + 4) + rr2 * __ldg(B + 5);
                     const double Sc = r0 * __ldg(B + 6) + r1 * __ldg(B + 7) + rr2 * __ldg(B + 8);
                     if constexpr (COMPUTE == 1) {
-                        sub += domain_sum_f32<SHAPE, WIDE, PDEG>(
+                        sub += domain_sum_f32<SHAPE, IDX, PDEG>(
                             P, reinterpret_cast<const ChunkF32*>(smem_raw),
                             reinterpret_cast<const float4*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
                     } else if constexpr (COMPUTE == 2) {
                         const double2* sch = reinterpret_cast<const double2*>(smem_raw);
-                        double a = domain_sum_f64_rec(P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src),
-                                                      Sa, Sb, Sc);
-                        if (!isfinite(a)) a = channel_sum_f64<0, true>(P, sch, Sa, Sb, Sc);  // limit branch
+                        double a = domain_sum_f64_rec<IDX>(
+                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), Sa, Sb, Sc);
+                        if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;
                     } else {
-                        sub += domain_sum_f64<SHAPE>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
+                        sub += domain_sum_f64<SHAPE, IDX>(P, reinterpret_cast<const double2*>(smem_raw), Sa, Sb, Sc);
                     }
                 }
                 acc += sub * factor;
@@ -589,9 +646,9 @@ __global__ void add_array_kernel(double* __restrict__ lhs, const float* __restri
 // ---------------------------------------------------------------------------
 // Host-side launchers (C++ linkage, used by nbx_runtime.cu).
 // ---------------------------------------------------------------------------
-template <int COMPUTE, int SHAPE, bool WIDE, int PDEG>
+template <int COMPUTE, int SHAPE, int IDX, int PDEG>
 static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) {
-    auto k = spots_kernel<COMPUTE, SHAPE, WIDE, PDEG>;
+    auto k = spots_kernel<COMPUTE, SHAPE, IDX, PDEG>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -602,34 +659,38 @@ static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) 
     return cudaGetLastError();
 }
 
-template <int COMPUTE, bool WIDE>
+template <int COMPUTE, int IDX>
 static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cudaStream_t st) {
     switch (shape) {
-        case 0: return launch_t<COMPUTE, 0, WIDE, kPolyF32>(P, smem, st);
-        case 1: return launch_t<COMPUTE, 1, WIDE, kPolyF32>(P, smem, st);
-        case 2: return launch_t<COMPUTE, 2, WIDE, kPolyF32>(P, smem, st);
-        default: return launch_t<COMPUTE, 3, WIDE, kPolyF32>(P, smem, st);
+        case 0: return launch_t<COMPUTE, 0, IDX, kPolyF32>(P, smem, st);
+        case 1: return launch_t<COMPUTE, 1, IDX, kPolyF32>(P, smem, st);
+        case 2: return launch_t<COMPUTE, 2, IDX, kPolyF32>(P, smem, st);
+        default: return launch_t<COMPUTE, 3, IDX, kPolyF32>(P, smem, st);
     }
 }
 
 // compute: 0 FP64, 1 FP32 (MUFU numerator), 2 FP32 with the degree-4 (ulp-grade) polynomial,
 // 5 FP32 degree-3 with the polynomial numerator (both sincg only), 4 FP64 with the channel
-// recurrence (sincg only)
-cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st) {
+// recurrence (sincg only).  idx: Fhkl index kind (kIdxMagic / kIdxWide / kIdxHash).
+cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st) {
     if (compute == 0) {
         const size_t smem = (size_t)P.n_src * 16;
-        return launch_shape<0, false>(P, shape, smem, st);
+        return idx == kIdxHash ? launch_shape<0, kIdxHash>(P, shape, smem, st)
+                               : launch_shape<0, kIdxWide>(P, shape, smem, st);
     }
     if (compute == 4) {  // FP64 channel recurrence (sincg)
         const size_t smem = (size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64);
-        return launch_t<2, 0, false, kPolyF32>(P, smem, st);
+        return idx == kIdxHash ? launch_t<2, 0, kIdxHash, kPolyF32>(P, smem, st)
+                               : launch_t<2, 0, kIdxWide, kPolyF32>(P, smem, st);
     }
     const size_t smem = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 16;  // n_src = channel pairs
+    if (idx == kIdxHash) return launch_shape<1, kIdxHash>(P, shape, smem, st);  // polynomial, scalar loop
+    const bool wide = idx == kIdxWide;
     if (compute == 2 && shape == 0)
-        return wide ? launch_t<1, 0, true, 4>(P, smem, st) : launch_t<1, 0, false, 4>(P, smem, st);
+        return wide ? launch_t<1, 0, kIdxWide, 4>(P, smem, st) : launch_t<1, 0, kIdxMagic, 4>(P, smem, st);
     if (compute == 5 && shape == 0)
-        return wide ? launch_t<1, 0, true, 5>(P, smem, st) : launch_t<1, 0, false, 5>(P, smem, st);
-    return wide ? launch_shape<1, true>(P, shape, smem, st) : launch_shape<1, false>(P, shape, smem, st);
+        return wide ? launch_t<1, 0, kIdxWide, 5>(P, smem, st) : launch_t<1, 0, kIdxMagic, 5>(P, smem, st);
+    return wide ? launch_shape<1, kIdxWide>(P, shape, smem, st) : launch_shape<1, kIdxMagic>(P, shape, smem, st);
 }
 
 static int grid_for(int64_t n, int block) {

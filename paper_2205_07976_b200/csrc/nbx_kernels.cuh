@@ -82,6 +82,16 @@ struct SpotsParams {
     const RunF64* runs;            // FP64 recurrence variant: uniform channel runs (sorted channels)
     int32_t n_runs;
     int32_t pad4;
+    // Sparse Fhkl (index kind 2, when the reachable Miller box is too large for a dense
+    // grid): open-addressing table of packed (h, k, l) -> F^2 (x sigma on FP32), empty
+    // slots ~0; misses and |index| >= 2^20 give default_f^2 (model.py:264-279).
+    const unsigned long long* hash_keys;
+    const void* hash_vals;         // float (FP32 path) / double (FP64 path)
+    uint32_t hash_mask;            // slots - 1 (power of two)
+    int32_t pad5;
+    double hash_def_d;
+    float hash_def_f;
+    float pad6;
 };
 
 }  // namespace nbx

@@ -23,7 +23,7 @@
 #include "nbx_poisson.h"
 
 namespace nbx {
-cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, bool wide, cudaStream_t st);
+cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
 cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
                             unsigned long long* fault, cudaStream_t st);
 cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStream_t st);
@@ -137,7 +137,9 @@ struct Plan {
                              // (NBX_FP32_POLY=4), 5 FP32 degree 3 with the polynomial numerator,
                              // 4 FP64 with the channel recurrence
     int shape = 0;
-    bool wide = false;
+    bool wide = false;        // dense grid with integer index (FP32 magic window exceeded)
+    bool hash = false;        // sparse Fhkl table (reachable box above kDenseMaxCells)
+    DevBuf hkeys, hvals;
     nbx::SpotsParams P{};
     DevBuf panels, bases, chan, chunks, table, runs;
     HostBuf host_table;       // pinned staging of the F^2 grid
@@ -363,6 +365,50 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
 }
 
 // Build (or, with `reuse`, rebuild in place -- its device buffers only grow) a plan.
+constexpr int64_t kDenseMaxCells = int64_t(1) << 26;
+
+// Sparse Fhkl table (index kind 2): open addressing, linear probing, at most half full;
+// the key packing and hash are the kernel's (nbx_kernels.cu:pack_hkl / hash_slot).  A
+// repeated (h, k, l) keeps its last amplitude.  Values are F^2 (x sigma on FP32).
+uint64_t pack_hkl_host(int h, int k, int l) {
+    return ((uint64_t)(uint32_t)(h + (1 << 20)) << 42) | ((uint64_t)(uint32_t)(k + (1 << 20)) << 21) |
+           (uint64_t)(uint32_t)(l + (1 << 20));
+}
+
+void build_hash(Plan* plan, const nbx_spots_desc* d, int compute, double def2, double sigma) {
+    uint64_t size = 1024;
+    while (size < 2 * (uint64_t)std::max(d->n_entries, 1)) size <<= 1;
+    if (size > (uint64_t(1) << 31)) throw ArgError("structure-factor table too large");
+    const uint32_t mask = (uint32_t)(size - 1);
+    std::vector<unsigned long long> keys(size, ~0ull);
+    std::vector<double> v64(size, 0.0);
+    for (int i = 0; i < d->n_entries; ++i) {
+        const uint64_t key = pack_hkl_host(d->hkl[3 * i], d->hkl[3 * i + 1], d->hkl[3 * i + 2]);
+        uint32_t s = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+        while (keys[s] != ~0ull && keys[s] != key) s = (s + 1) & mask;
+        keys[s] = key;
+        v64[s] = d->amplitudes[i] * d->amplitudes[i];
+    }
+    plan->hkeys.ensure(size * sizeof(unsigned long long));
+    NBX_CUDA(cudaMemcpy(plan->hkeys.p, keys.data(), size * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    nbx::SpotsParams& P = plan->P;
+    if (compute == NBX_COMPUTE_FP32) {
+        std::vector<float> v32(size);
+        for (uint64_t i = 0; i < size; ++i) v32[i] = (float)(v64[i] * sigma);
+        plan->hvals.ensure(size * sizeof(float));
+        NBX_CUDA(cudaMemcpy(plan->hvals.p, v32.data(), size * sizeof(float), cudaMemcpyHostToDevice));
+    } else {
+        plan->hvals.ensure(size * sizeof(double));
+        NBX_CUDA(cudaMemcpy(plan->hvals.p, v64.data(), size * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    P.hash_keys = static_cast<const unsigned long long*>(plan->hkeys.p);
+    P.hash_vals = plan->hvals.p;
+    P.hash_mask = mask;
+    P.hash_def_d = def2;
+    P.hash_def_f = (float)(def2 * sigma);
+    plan->info.table_cells = (int64_t)size;
+}
+
 // NBX_TRACE: wall time of the phases of a plan build, printed to stderr.
 struct PhaseTimer {
     bool on = trace_enabled();
@@ -391,6 +437,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         plan->P = nbx::SpotsParams{};
         plan->info = nbx_plan_info_t{};
         plan->wide = false;
+        plan->hash = false;
         plan->last_ms = -1.f;
     }
     try {
@@ -442,24 +489,27 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         double ivmax = 0.0;
         for (int i = sb; i < se; ++i) ivmax = std::max(ivmax, 1.0 / d->wavelengths[i]);
         int hmax[3];
+        bool huge = false;
         for (int a = 0; a < 3; ++a) {
             double m = 0.0;
             for (int dd = 0; dd < d->n_domains; ++dd) m = std::max(m, norm3(d->bases + 9 * dd + 3 * a));
             const double hb = std::ceil(m * relmax * ivmax) + 1.0;
-            if (hb > (double)(1 << 20)) throw ArgError("reachable Miller range exceeds the supported |index| < 2^20");
-            hmax[a] = (int)hb;
+            huge |= hb > (double)(1 << 20);
+            hmax[a] = (int)std::min(hb, (double)(1 << 20));
         }
         const int64_t dims[3] = {2 * (int64_t)hmax[0] + 1, 2 * (int64_t)hmax[1] + 1, 2 * (int64_t)hmax[2] + 1};
         const int64_t cells = dims[0] * dims[1] * dims[2];
-        if (cells > (int64_t(1) << 30))
-            throw ArgError("reachable Miller box too large for the dense Fhkl grid (" + std::to_string(cells) +
-                           " cells)");
+        // Dense grid up to kDenseMaxCells (64M cells: every protein-sized cell at any
+        // resolution the detector reaches); beyond it (virus-sized cells) a sparse table.
+        const char* hev = std::getenv("NBX_FHKL_HASH");
+        plan->hash = huge || cells > kDenseMaxCells || (hev && std::atoi(hev) == 1);
+        if (plan->hash && compute == NBX_COMPUTE_FP32) plan->kernel_variant = 5;  // scalar polynomial loop
         for (int a = 0; a < 3; ++a) P.lo[a] = -hmax[a];
         P.sK = (int32_t)dims[2];
         P.sH = (int32_t)(dims[1] * dims[2]);
-        int64_t cells_alloc = cells;
+        int64_t cells_alloc = plan->hash ? 0 : cells;
         plan->wide = false;
-        if (compute == NBX_COMPUTE_FP32) {
+        if (compute == NBX_COMPUTE_FP32 && !plan->hash) {
             // FP32 index: power-of-two strides so that the cell number is two shift-adds
             // of the magic-rounded floats' bit patterns (ALU pipe, no FMA-pipe work):
             //   bits(mA) << lg(sH) + bits(mB) << lg(sK) + bits(mC) = cell + c (mod 2^32),
@@ -492,8 +542,8 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         // into pinned staging memory: first the largest reachable F^2, then the fill
         const double def2 = d->default_f * d->default_f;
         auto reachable = [&](int i) {
-            return std::abs(d->hkl[3 * i]) <= hmax[0] && std::abs(d->hkl[3 * i + 1]) <= hmax[1] &&
-                   std::abs(d->hkl[3 * i + 2]) <= hmax[2];
+            return plan->hash || (std::abs(d->hkl[3 * i]) <= hmax[0] && std::abs(d->hkl[3 * i + 1]) <= hmax[1] &&
+                                  std::abs(d->hkl[3 * i + 2]) <= hmax[2]);
         };
         auto cell_of = [&](int i) {
             return (int64_t)(d->hkl[3 * i] + hmax[0]) * P.sH + (int64_t)(d->hkl[3 * i + 1] + hmax[1]) * P.sK +
@@ -529,10 +579,12 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         }
         // device table still current: same entries, grid and scale, buffer not reallocated
         const size_t tbytes = (size_t)cells_alloc * (compute == NBX_COMPUTE_FP32 ? sizeof(float) : sizeof(double));
-        const bool table_current = same_entries && tk.sigma == sigma && tk.dev == plan->table.p &&
+        const bool table_current = !plan->hash && same_entries && tk.sigma == sigma && tk.dev == plan->table.p &&
                                    plan->table.bytes >= tbytes;
         if (!table_current) tk.valid = false;  // re-armed after the upload below
-        if (table_current) {
+        if (plan->hash) {
+            build_hash(plan, d, compute, def2, sigma);
+        } else if (table_current) {
             // nothing to fill or upload
         } else if (compute == NBX_COMPUTE_FP32) {
             float* tf = plan->host_table.ensure<float>(cells_alloc);
@@ -600,7 +652,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                                 cudaMemcpyHostToDevice));
             P.chunks = static_cast<const nbx::ChunkF32*>(plan->chunks.p);
             P.n_chunks = (int32_t)chunks.size();
-            if (!table_current) {
+            if (!table_current && !plan->hash) {
                 plan->table.ensure(cells_alloc * sizeof(float));
                 NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells_alloc * sizeof(float),
                                     cudaMemcpyHostToDevice));
@@ -657,13 +709,13 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                 P.runs = static_cast<const nbx::RunF64*>(plan->runs.p);
                 P.n_runs = (int32_t)runs.size();
             }
-            if (!table_current) {
+            if (!table_current && !plan->hash) {
                 plan->table.ensure(cells * sizeof(double));
                 NBX_CUDA(cudaMemcpy(plan->table.p, plan->host_table.p, cells * sizeof(double),
                                     cudaMemcpyHostToDevice));
             }
         }
-        if (!table_current) {
+        if (!table_current && !plan->hash) {
             tk.compute = compute;
             tk.default_f = d->default_f;
             tk.sH = P.sH;
@@ -711,13 +763,13 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         nbx_plan_info_t& I = plan->info;
         I.n_pixels = plan->n_pixels;
         I.steps = plan->steps;
-        I.table_cells = cells_alloc;
+        if (!plan->hash) I.table_cells = cells_alloc;  // hash: build_hash recorded the slot count
         for (int a = 0; a < 3; ++a) {
             I.table_lo[a] = P.lo[a];
             I.table_dim[a] = (int32_t)dims[a];
         }
         I.compute = compute;
-        I.table_kind = plan->wide ? 1 : 0;
+        I.table_kind = plan->hash ? 2 : (plan->wide ? 1 : 0);
         I.channel_runs = P.n_runs;
         I.kernel_variant = plan->kernel_variant;
         I.scale = plan->scale;
@@ -758,7 +810,7 @@ void launch_rows(Plan* plan, int mode, void* dout, unsigned long long* fault, cu
     P.fault_bg = fault + 1;  // fault_bg[1] = the downcast slot
     P.row0 = row0;
     P.max_slow = row1;
-    NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->wide, st));
+    NBX_CUDA(nbx::launch_spots(P, plan->kernel_variant, plan->shape, plan->hash ? 2 : (plan->wide ? 1 : 0), st));
 }
 
 // Enqueue one spot launch of `plan` into device buffer `dout` with fault slots `fault`.

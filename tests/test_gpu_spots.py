@@ -396,6 +396,47 @@ def test_reused_plan_tracks_table_changes(gpu, compute):
         assert np.array_equal(got, fresh)
 
 
+@pytest.mark.parametrize("name", ["scalar_match", "triclinic_pol_2wl", "c1_toy", "ls49_centre", "ls49_edge"])
+def test_sparse_fhkl_table_matches_reference(gpu, monkeypatch, name):
+    """The sparse (hash) Fhkl table -- used when the reachable Miller box exceeds the dense
+    grid limit -- forced on the reference fixtures: FP64 bit-identical to the dense grid (same
+    F^2 values, same lookups), both paths within their tolerances of the reference."""
+    monkeypatch.setenv("NBX_FHKL_HASH", "1")
+    case = parity.load(name)
+    plan = SpotsPlan(parity.context(case, "fp64"))
+    assert plan.info.table_kind == 2
+    got64 = run(parity.context(case, "fp64"), "f64").data
+    m = parity.metrics(got64, case["ref_f64"], dims(case))
+    assert m["total"] < FP64_TOL and m["spot"] < FP64_TOL and m["pix_abs_over_max"] < FP64_TOL, m
+    got32 = run(parity.context(case, "fp32"), "f32").data
+    m = parity.metrics(got32, case["ref_f64"], dims(case))
+    assert m["total"] < FP32_TOL and m["spot"] < FP32_TOL, m
+    monkeypatch.delenv("NBX_FHKL_HASH")
+    assert np.array_equal(got64, run(parity.context(case, "fp64"), "f64").data)
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_virus_sized_cell_uses_sparse_table(gpu, compute):
+    """A 900 A cubic cell reaches |h| ~ 600 on the C2 detector corner: a dense box of ~2e9
+    cells.  The plan switches to the sparse table instead of failing; checked against the
+    CPU oracle (searchsorted lookup, any index) on a high-resolution ROI."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import CrystalModel, MosaicDomainSet, StructureFactorTable, UnitCell
+
+    rng = np.random.default_rng(3)
+    hkl = rng.integers(-400, 401, size=(20000, 3))
+    entries = {tuple(int(v) for v in h): float(a) for h, a in zip(hkl, rng.uniform(10, 300, len(hkl)))}
+    panel = synthetic.roi(synthetic.rayonix_panel(), 60, 200, 12, 16)
+    base = synthetic.ls49_context(panel=panel, n_channels=3, n_domains=2, compute=compute)
+    crystal = CrystalModel(UnitCell(900, 900, 900, 90, 90, 90), base.crystal.orientation, (5, 5, 5),
+                           MosaicDomainSet(base.crystal.mosaic.rotations), StructureFactorTable(entries, 1.0))
+    ctx = dataclasses.replace(base, crystal=crystal)
+    plan = SpotsPlan(ctx)
+    assert plan.info.table_kind == 2
+    oracle_check(ctx, FP64_TOL if compute == "fp64" else FP32_TOL)
+
+
 def test_add_array_upcast_semantics(gpu):
     lhs = PixelBuffer((1, 3), "f64", [0.0, 1.0, 2.0])
     rhs = PixelBuffer((1, 3), "f32", [0.1, 0.5, 0.25])
