@@ -380,3 +380,14 @@ def poisson_host(buf: PixelBuffer, seed: int, image: int = 0) -> PixelBuffer:
     if status != N.NBX_OK:
         raise ValueError("invalid poisson_host arguments")
     return out
+
+
+def __getattr__(name):
+    # image_stats / image_histogram live in xtrace.kernels (kernels.py:334-430); here they are
+    # implemented next to the image I/O (io.py) and re-exported lazily (io imports this module)
+    if name in ("image_stats", "image_histogram", "ImageStats", "HistogramResult"):
+        from . import io
+
+        return getattr(io, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+
