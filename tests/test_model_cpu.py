@@ -185,3 +185,24 @@ def test_background_interp_and_validation_equal_reference():
         with pytest.raises(Exception) as e_ours:
             BackgroundProfile(points=bad)
         assert type(e_ours.value).__name__ == type(e_ref.value).__name__
+
+
+def test_public_names_cover_the_reference_spot_api():
+    """Every public name of xtrace.model / xtrace.kernels exists here (DESIGN.md §9 lists the
+    out-of-scope top-level names, which are the only ones allowed to be missing)."""
+    ref()
+    import xtrace
+    import xtrace.kernels as xk
+    import xtrace.model as xm
+
+    import paper_2205_07976_b200 as ours
+    import paper_2205_07976_b200.kernels as ok
+
+    assert not set(xm.__all__) - set(dir(mm))
+    assert not {n for n in xk.__all__ if not hasattr(ok, n)}
+    out_of_scope = {"CampaignIOError", "CampaignPlan", "CampaignReport", "ConfigError", "ParseError", "RangePolicy",
+                    "ScalingRow", "SimulationConfig", "default_worker_count", "kernel_time_table", "load_background",
+                    "load_config", "load_hkl", "parallel_for", "parallel_reduce", "parallel_scan", "scheduler",
+                    "strong_scaling", "write_preview", "write_scaling_csv"}
+    public = {n for n in dir(xtrace) if not n.startswith("_")}
+    assert public - set(dir(ours)) <= out_of_scope, sorted(public - set(dir(ours)) - out_of_scope)
