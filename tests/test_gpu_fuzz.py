@@ -2,7 +2,8 @@
 
 Each case draws a triclinic cell and orientation, a tilted / off-axis panel (sometimes a
 two-panel detector with thickness layers), a spectrum that is uniform in 1/lambda or random,
-mosaic domains, oversampling, crystal size and Fhkl table, so the plan's choices -- FP32
+mosaic domains, oversampling, crystal size, Fhkl table, shape transform and phi scan, so the
+plan's choices -- FP32
 MUFU vs polynomial numerator, FP32 chunking, FP64 recurrence runs vs direct kernel, dense
 vs sparse Fhkl, row-banded host download -- are all exercised against the same independent
 checker.  Tolerances: FP64 1e-9, FP32 1e-4 on total and every spot.
@@ -15,7 +16,7 @@ import pytest
 
 import parity
 from oracle import oracle
-from paper_2205_07976_b200 import (BeamSpectrum, CrystalModel, Detector, DetectorPanel, Orientation, PixelBuffer,
+from paper_2205_07976_b200 import (BeamSpectrum, CrystalModel, Detector, DetectorPanel, Orientation, PhiScan, PixelBuffer,
                                    SpotsContext, SpotsPlan, StructureFactorTable, UnitCell, describe,
                                    generate_mosaic_rotations, nanobragg_spots, synthetic)
 
@@ -63,7 +64,10 @@ def random_case(seed: int) -> SpotsContext:
         panel = Detector(panels)
     else:
         panel = DetectorPanel(rows, cols, px, dist, bc, fast_axis=fast, slow_axis=slow)
-    return SpotsContext(crystal, panel, spec, oversample=int(rng.integers(1, 4)))
+    shape = "sincg" if rng.random() < 0.75 else str(rng.choice(["gauss", "round", "tophat"]))
+    phi = PhiScan(float(rng.uniform(-5, 5)), float(rng.uniform(0, 0.5)), int(rng.integers(1, 4)),
+                  tuple(synthetic.random_rotation(rng)[0])) if rng.random() < 0.25 else None
+    return SpotsContext(crystal, panel, spec, oversample=int(rng.integers(1, 4)), shape=shape, phi=phi)
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("NBX_FUZZ_CASES", "32"))))
@@ -74,6 +78,12 @@ def test_random_configuration_vs_oracle(gpu, seed):
         c = dataclasses.replace(ctx, compute=compute)
         out = PixelBuffer.zeros(c.panel.dims, "f64")
         nanobragg_spots(c, out)
-        m = parity.metrics(out.data, want, c.panel.dims)
         info = SpotsPlan(c).info
+        if compute == "fp32" and want.sum() < 1e-30:
+            # physically empty image (e.g. a Gaussian transform far from every lattice point:
+            # ~1e-96 photons): below FP32's range relative to the sigma-scaled peak the FP32
+            # path returns ~0; only the absolute agreement is meaningful there
+            assert np.abs(out.data - want).max() < 1e-30, (seed, info.kernel_variant)
+            continue
+        m = parity.metrics(out.data, want, c.panel.dims)
         assert m["total"] < tol and m["spot"] < tol, (compute, seed, info.kernel_variant, info.table_kind, m)
