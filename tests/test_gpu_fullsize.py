@@ -17,7 +17,7 @@ import pytest
 
 import parity
 from oracle import oracle
-from paper_2205_07976_b200 import PixelBuffer, SpotsPlan, describe, synthetic
+from paper_2205_07976_b200 import DetectorPanel, PixelBuffer, SpotsPlan, describe, nanobragg_spots, synthetic
 from paper_2205_07976_b200 import _native as N
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -87,3 +87,23 @@ def test_c4_shaped_detector_vs_oracle(gpu):
     nanobragg_spots(ctx, out)
     m = parity.metrics(out.data, want, det.dims)
     assert m["total"] < 1e-9 and m["spot"] < 1e-9, m
+
+
+@pytest.mark.parametrize("compute", ["fp32", "fp64"])
+def test_large_8k_image_bands_and_offsets(gpu, compute):
+    """8192 x 8192 pixels (67M: int64 output offsets, 8 row bands of 1024 rows through the
+    pipelined host download): rows taken from the full image equal the same rows rendered as
+    a sub-panel, bit for bit, at the top, the middle and the bottom."""
+    import dataclasses
+
+    base = DetectorPanel(8192, 8192, 40e-6, 0.2, (4095.5, 4095.5))
+    ctx = synthetic.ls49_context(panel=base, n_channels=2, n_domains=1, compute=compute)
+    full = PixelBuffer.zeros(base.dims, "f32")
+    nanobragg_spots(ctx, full)
+    img = full.data.reshape(base.dims)
+    assert np.isfinite(img).all() and img.max() > 0
+    for r0 in (0, 4090, 8185):
+        sub = synthetic.roi(base, r0, 0, 7, 8192)
+        out = PixelBuffer.zeros(sub.dims, "f32")
+        nanobragg_spots(dataclasses.replace(ctx, panel=sub), out)
+        assert np.array_equal(out.data.reshape(sub.dims), img[r0:r0 + 7])
