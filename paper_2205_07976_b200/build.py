@@ -55,17 +55,22 @@ def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | N
         return LIB
     lib.parent.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(exist_ok=True)
-    objs = []
-    logs = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = lib.parent / (lib.stem + "_" + Path(src).stem + ".o")
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *(extra_flags or []), "-I", str(ROOT / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(res.stderr)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{res.stderr}")
-        objs.append(str(obj))
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    logs = []
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:  # the translation units compile in parallel
+        for src, obj, res in pool.map(compile_one, SOURCES):
+            logs.append(res.stderr)
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {src}:\n{res.stderr}")
+            objs.append(str(obj))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
