@@ -38,3 +38,40 @@ def test_channel_sharded_two_ranks(gpu):
     d = torchrun(["--mode", "channels", "--channels", "64", "--steps", "2", "--warmup", "3", "--size", "512"], 29532)
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["images_per_gpu_per_step"] == 0.5
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+CAMPAIGN_SCRIPT = r'''
+import os, sys, json
+sys.path.insert(0, os.environ["NBX_ROOT"])
+import torch.distributed as dist
+from paper_2205_07976_b200 import synthetic
+from paper_2205_07976_b200.io import run_campaign, read_image
+dist.init_process_group("gloo")
+panel = synthetic.roi(synthetic.rayonix_panel(), 1800, 1800, 48, 64)
+ctx_for = lambda i: synthetic.ls49_context(synthetic.SEED + i, panel=panel, n_channels=4, n_domains=2)
+res = run_campaign(ctx_for, 7, sys.argv[1], first_image=3)
+print(json.dumps({"rank": dist.get_rank(), "indices": res.indices, "crcs": res.crcs}), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_campaign_sharded_over_two_ranks(gpu, tmp_path):
+    """run_campaign under torchrun (SURVEY §8 E1/F3): each rank renders a contiguous share of
+    the 7 images (plan_batches: 4 + 3), the shares cover every index once, and every image
+    equals a one-rank campaign's bit for bit (same CRC)."""
+    script = tmp_path / "camp.py"
+    script.write_text(CAMPAIGN_SCRIPT)
+    env = dict(os.environ, NBX_ROOT=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29533", str(script), str(tmp_path / "two")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rows = sorted((json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")), key=lambda r: r["rank"])
+    assert [r["indices"] for r in rows] == [[3, 4, 5, 6], [7, 8, 9]]
+    crc2 = {i: c for r in rows for i, c in zip(r["indices"], r["crcs"])}
+    one = subprocess.run([sys.executable, str(script), str(tmp_path / "one")], capture_output=True, text=True,
+                         timeout=600, env=dict(env, RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                                               MASTER_PORT="29534"))
+    assert one.returncode == 0, one.stderr[-3000:]
+    r1 = json.loads([ln for ln in one.stdout.splitlines() if ln.startswith("{")][0])
+    assert dict(zip(r1["indices"], r1["crcs"])) == crc2
