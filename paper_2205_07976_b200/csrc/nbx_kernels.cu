@@ -563,8 +563,8 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
             bad = !isfinite(v);
             break;
         }
-        case kOutRawF64: {  // raw partial for channel shards
-            static_cast<double*>(P.out)[p] += acc;
+        case kOutRawF64: {  // raw partial for channel shards (sigma removed: shards' sigmas differ)
+            static_cast<double*>(P.out)[p] += acc * P.raw_scale;
             break;
         }
         default: {  // kOutImageF64/F32: simulate_image's accumulator, spots (+ background) fused

@@ -67,6 +67,7 @@ struct SpotsParams {
     int32_t sh_h, sh_k;            // FP32: log2 of the power-of-two strides
     uint32_t lea_bias;             // FP32: 0x4B400000 (sH + sK + 1) mod 2^32
     double out_scale;              // r_e^2 fluence / norm (/ sigma on the FP32 path)
+    double raw_scale;              // 1 / sigma (exact power of two): RAW partials are sigma-free
     void* out;
     unsigned long long* fault;     // lowest non-finite pixel (atomicMin), ~0ull when none
     int32_t max_slow, max_fast;    // launch covers rows [row0, max_slow) of every panel

@@ -121,6 +121,7 @@ struct Ctx {
     cudaEvent_t join_ev = nullptr;
     DevBuf out_scratch;     // device image when the caller passes host memory
     DevBuf stage_in, stats_parts, stats_res, hist_counts;  // image_stats / image_histogram scratch
+    DevBuf raw_scratch;     // FP64 partial of a long spectrum split into channel shards
     DevBuf fault;           // one u64
     std::string err;
 };
@@ -757,6 +758,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         P.max_slow = max_slow;
         P.max_fast = max_fast;
         P.out_scale = plan->out_scale;
+        P.raw_scale = 1.0 / sigma;
         setup_background(d, P, plan->bg);
 
         pt.mark("rest");
@@ -1041,6 +1043,7 @@ void nbx_ctx_destroy(void* ctxp) {
     ctx->stats_parts.release();
     ctx->stats_res.release();
     ctx->hist_counts.release();
+    ctx->raw_scratch.release();
     ctx->fault.release();
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1120,9 +1123,60 @@ void nbx_plan_destroy(void* planp) {
     delete plan;
 }
 
+int nbx_finalize(void* ctxp, const double* raw, int64_t n, double scale, int out_mode, void* out, int out_on_device,
+                 int64_t* first_bad);
+
+// Sources per launch when a spectrum is too long for one kernel's shared-memory channel table.
+constexpr int kMaxShardSources = 8192;
+
 int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, void* out, int out_on_device,
               int64_t* first_bad) {
     int64_t bad = -1;
+    if (ctxp && d && d->n_sources > 0) {
+        const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
+        if (se - sb > kMaxShardSources && out_mode != NBX_OUT_IMAGE_F64 && out_mode != NBX_OUT_IMAGE_F32) {
+            // Long spectrum (the reference has no limit): channel shards accumulated as FP64
+            // partials with the GLOBAL normalisation, then one scale + store -- exactly a
+            // channel-sharded image on one device.  A RAW request receives
+            // the shards' partials added into the caller's buffer.
+            int64_t npix = 0;
+            double scale = 0.0;
+            const int st = guarded(ctxp, [&] {
+                Ctx* ctx = static_cast<Ctx*>(ctxp);
+                NBX_CUDA(cudaSetDevice(ctx->device));
+                check_mode(out_mode);
+                validate(d);
+                npix = count_pixels(d);
+                nbx_spots_desc sh = *d;
+                if (!(sh.norm > 0)) {  // kernels.py:243-245 over the WHOLE spectrum
+                    double wsum = 0.0;
+                    for (int i = 0; i < d->n_sources; ++i) wsum += d->weights[i];
+                    sh.norm = wsum * (double)d->n_domains * (double)(d->oversample * d->oversample);
+                }
+                const bool raw_out = out_mode == NBX_OUT_RAW_F64;
+                void* acc = out;
+                int acc_on_device = out_on_device;
+                if (!raw_out) {
+                    ctx->raw_scratch.ensure((size_t)npix * sizeof(double));
+                    NBX_CUDA(cudaMemsetAsync(ctx->raw_scratch.p, 0, (size_t)npix * sizeof(double), ctx->stream));
+                    acc = ctx->raw_scratch.p;
+                    acc_on_device = 1;
+                }
+                if (!ctx->oneshot) ctx->oneshot = new Plan();
+                for (int s0 = sb; s0 < se; s0 += kMaxShardSources) {
+                    sh.src_begin = s0;
+                    sh.src_end = std::min(se, s0 + kMaxShardSources);
+                    Plan* plan = build_plan(ctx, &sh, compute, ctx->oneshot);
+                    scale = plan->scale;
+                    run_plan(plan, NBX_OUT_RAW_F64, acc, acc_on_device);  // += this shard's partial
+                }
+                return NBX_OK;
+            });
+            if (st != NBX_OK || out_mode == NBX_OUT_RAW_F64) return st;
+            return nbx_finalize(ctxp, static_cast<const double*>(static_cast<Ctx*>(ctxp)->raw_scratch.p), npix, scale,
+                                out_mode, out, out_on_device, first_bad);
+        }
+    }
     int st = guarded(ctxp, [&] {
         if (!ctxp) throw ArgError("NULL context");
         NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
