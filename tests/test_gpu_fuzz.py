@@ -87,3 +87,29 @@ def test_random_configuration_vs_oracle(gpu, seed):
             continue
         m = parity.metrics(out.data, want, c.panel.dims)
         assert m["total"] < tol and m["spot"] < tol, (compute, seed, info.kernel_variant, info.table_kind, m)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_channel_shards_sum_to_whole(gpu, seed):
+    """The channel-sharded decomposition (C5) on random configurations: FP64 partials of random
+    source shards, summed and scaled once, equal the whole image (both paths)."""
+    from paper_2205_07976_b200 import _native as N
+
+    ctx = random_case(100 + seed)
+    n_src = len(ctx.spectrum.samples)
+    if n_src < 2:
+        pytest.skip("one source")
+    cut = int(np.random.default_rng(seed).integers(1, n_src))
+    for compute, rtol in (("fp64", 1e-11), ("fp32", 1e-4)):
+        c = dataclasses.replace(ctx, compute=compute)
+        whole = PixelBuffer.zeros(c.panel.dims, "f64")
+        nanobragg_spots(c, whole)
+        if compute == "fp32" and whole.data.sum() < 1e-30:
+            continue  # physically empty image (see test_random_configuration_vs_oracle)
+        plan = SpotsPlan(c)
+        raw = np.zeros(plan.n_pixels)
+        for lo, hi in ((0, cut), (cut, n_src)):
+            SpotsPlan(c, src_begin=lo, src_end=hi, norm=0.0).run(raw, mode=N.OUT_RAW_F64)
+        got = raw * plan.scale
+        m = parity.metrics(got, whole.data, c.panel.dims)
+        assert m["total"] < rtol and m["spot"] < rtol, (compute, seed, cut, m)
