@@ -458,6 +458,28 @@ def test_long_spectrum_is_channel_sharded_on_one_device(gpu, compute):
     np.testing.assert_allclose(f32, got, rtol=2.0 ** -23, atol=0)
 
 
+def test_pipelined_image_mode_with_background_is_bitwise_the_device_image(gpu):
+    """simulate_image's fused spots + background accumulator (NBX_OUT_IMAGE_F64) through the
+    banded host download equals the single-launch device-output image bit for bit."""
+    import torch
+
+    from paper_2205_07976_b200 import BackgroundProfile, _native as N
+
+    water = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.3, 6.5)))
+    panel = synthetic.roi(synthetic.rayonix_panel(), 1400, 1400, 1030, 1024)
+    ctx = synthetic.ls49_context(panel=panel, n_channels=3, n_domains=2, compute="fp32")
+    desc = describe(ctx, background=water, thickness_factor=0.8)
+    cx = N.context()
+    dev = torch.zeros(panel.n_pixels, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    bad = N.C.c_int64(-1)
+    assert cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), 1, N.OUT_IMAGE_F64, dev.data_ptr(), 1, N.C.byref(bad)) == 0
+    host = np.full(panel.n_pixels, np.nan)
+    assert cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), 1, N.OUT_IMAGE_F64, host.ctypes.data, 0,
+                            N.C.byref(bad)) == 0
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
 def test_add_array_upcast_semantics(gpu):
     lhs = PixelBuffer((1, 3), "f64", [0.0, 1.0, 2.0])
     rhs = PixelBuffer((1, 3), "f32", [0.1, 0.5, 0.25])
