@@ -7,8 +7,18 @@
 // table (1/lambda, weight) is staged once per block in shared memory and read
 // with one 16-byte LDS per step; rotated bases are warp-uniform __ldg loads
 // amortised over the channel loop.  Per-pixel accumulation is strictly
-// sequential, so the image is bitwise independent of launch geometry and
-// block order (test_kernels.py:208-246 contract).
+// sequential, so the image is bitwise independent of launch geometry, block
+// order and the row bands of a pipelined run (test_kernels.py:208-246 contract).
+//
+// Variants (spots_kernel<COMPUTE, SHAPE, IDX, PDEG>, chosen per plan by the host):
+//   COMPUTE 1 FP32 path: PDEG 3 = packed-pair loop with the MUFU.SIN numerator (the
+//     throughput kernel), 5 = same loop with the polynomial numerator (few samples
+//     per pixel), 4 = degree-4 polynomials; non-grating shapes and the wide / hash
+//     Fhkl indices take the scalar loop.
+//   COMPUTE 0 FP64 path, direct per-channel evaluation; COMPUTE 2 FP64 path with the
+//     channel recurrence (uniform 1/lambda runs).
+//   IDX: Fhkl index kind -- magic-float bit patterns on a power-of-two grid, integer
+//     index on a dense grid, or the sparse hash table.
 #include <cuda_runtime.h>
 #include <cstdint>
 
