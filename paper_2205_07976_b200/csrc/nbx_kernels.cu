@@ -235,7 +235,10 @@ __device__ __forceinline__ float chunk_sum_f32x2(const SpotsParams& P, const flo
                             __float_as_uint(lo2(C.m));
         const uint32_t c1 = (__float_as_uint(hi2(A.m)) << P.sh_h) + (__float_as_uint(hi2(B.m)) << P.sh_k) +
                             __float_as_uint(hi2(C.m));
-        const f2x F2 = pk2(__ldg(base + c0), __ldg(base + c1));
+        // the F^2 gather through the texture path: a 32-bit element index (the bias folds into the
+        // index adds) instead of 64-bit address arithmetic -- 2.4 fewer ALU issues per channel
+        const f2x F2 = pk2(tex1Dfetch<float>(P.table_tex, (int)(c0 - P.lea_bias)),
+                           tex1Dfetch<float>(P.table_tex, (int)(c1 - P.lea_bias)));
         acc = fma2(mul2(F2, W), L2, acc);
     }
     return lo2(acc) + hi2(acc);

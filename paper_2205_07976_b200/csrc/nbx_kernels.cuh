@@ -93,6 +93,7 @@ struct SpotsParams {
     double hash_def_d;
     float hash_def_f;
     float pad6;
+    unsigned long long table_tex;  // FP32 power-of-two table as a texture object (the packed loop's gather)
 };
 
 }  // namespace nbx

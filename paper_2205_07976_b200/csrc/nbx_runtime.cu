@@ -140,6 +140,16 @@ struct Plan {
     int shape = 0;
     bool wide = false;        // dense grid with integer index (FP32 magic window exceeded)
     bool hash = false;        // sparse Fhkl table (reachable box above kDenseMaxCells)
+    cudaTextureObject_t tex = 0;  // texture view of `table` (FP32 power-of-two grid)
+    const void* tex_ptr = nullptr;
+    size_t tex_bytes = 0;
+    void release_tex() {
+        if (tex) cudaDestroyTextureObject(tex);
+        tex = 0;
+        tex_ptr = nullptr;
+        tex_bytes = 0;
+    }
+    ~Plan() { release_tex(); }
     DevBuf hkeys, hvals;
     nbx::SpotsParams P{};
     DevBuf panels, bases, chan, chunks, table, runs;
@@ -755,6 +765,24 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         P.nnn_f = (float)P.nnn_d;
         P.pol_on = d->polarization_on ? 1 : 0;
         P.table = plan->table.p;
+        if (compute == NBX_COMPUTE_FP32 && !plan->hash && !plan->wide) {
+            // texture view of the power-of-two table for the packed loop's gathers
+            const size_t tb = (size_t)cells_alloc * sizeof(float);
+            if (!plan->tex || plan->tex_ptr != plan->table.p || plan->tex_bytes != tb) {
+                plan->release_tex();
+                cudaResourceDesc rd{};
+                rd.resType = cudaResourceTypeLinear;
+                rd.res.linear.devPtr = plan->table.p;
+                rd.res.linear.desc = cudaCreateChannelDesc<float>();
+                rd.res.linear.sizeInBytes = tb;
+                cudaTextureDesc td{};
+                td.readMode = cudaReadModeElementType;
+                NBX_CUDA(cudaCreateTextureObject(&plan->tex, &rd, &td, nullptr));
+                plan->tex_ptr = plan->table.p;
+                plan->tex_bytes = tb;
+            }
+            P.table_tex = plan->tex;
+        }
         P.max_slow = max_slow;
         P.max_fast = max_fast;
         P.out_scale = plan->out_scale;
