@@ -55,6 +55,8 @@ def parse():
                     help="image: C2 image-sharded (default); channels: C5 one 1000-channel image channel-sharded; "
                          "jungfrau: C4 256-panel FP64")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / fp64 / cpu-baseline legs")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="channels mode: NCCL reduce of the partials (default) or fused peer-memory slots")
     return ap.parse_args()
 
 
@@ -201,6 +203,17 @@ def run_ours(args):
             c = ctx_for(i, args.compute)
             plans.append(SpotsPlan(c, device=local, src_begin=lo, src_end=hi, norm=parallel.global_norm(c)))
         raw = torch.zeros(plans[0].n_pixels, dtype=torch.float64, device="cuda")
+        slots = None
+        if args.transport == "p2p" and world > 1:  # root's IPC slots, mapped once by every rank
+            slots = N.C.c_void_p()
+            handle = [None]
+            if rank == 0:
+                hb = N.C.create_string_buffer(64)
+                N.check(cx, cx.lib.nbx_ipc_alloc(cx.handle, world * plans[0].n_pixels * 8, N.C.byref(slots), hb))
+                handle = [bytes(hb.raw)]
+            dist.broadcast_object_list(handle, src=0)
+            if rank != 0:
+                N.check(cx, cx.lib.nbx_ipc_open(cx.handle, handle[0], N.C.byref(slots)))
     else:
         plans = [SpotsPlan(ctx_for(i, args.compute), device=local) for i in range(n_img)]
     steps_per_unit = plans[0].steps  # per rank per step
@@ -215,6 +228,16 @@ def run_ours(args):
         flush.zero_()
         if mode != "channels":
             plans[i].run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            return
+        if slots is not None:  # fused: the kernel stores this rank's partial into the root's slot
+            plans[i].run(slots.value + rank * plans[i].n_pixels * 8, mode=N.OUT_RAW_STORE_F64, on_device=True)
+            dist.barrier()
+            if rank == 0:
+                bad = N.C.c_int64(-1)
+                st = cx.lib.nbx_reduce_slots(cx.handle, slots.value, world, plans[i].n_pixels, plans[i].scale,
+                                             N.OUT_F32, out.data_ptr(), 1, N.C.byref(bad))
+                N.check(cx, st, bad.value)
+            dist.barrier()
             return
         raw.zero_()
         plans[i].run(raw.data_ptr(), mode=N.OUT_RAW_F64, on_device=True)
@@ -265,12 +288,15 @@ def run_ours(args):
             traffic = None
     workload = {"image": WORKLOAD if size == 3840 else f"{WORKLOAD} (ROI {size}x{size})",
                 "channels": f"C5 single LS49-shape image, {size}x{size}, {args.channels} channels (7020 + 0.2 j eV), "
-                            f"{args.domains} mosaic domains, channel-sharded over {world} GPU(s) + NCCL reduce",
+                            f"{args.domains} mosaic domains, channel-sharded over {world} GPU(s) + "
+                            f"{'peer-memory slots' if args.transport == 'p2p' else 'NCCL reduce'}",
                 "jungfrau": f"C4 Jungfrau-16M-like: 256 panels x 254x254, oversample 2, 3 thickness layers, "
                             f"{args.channels} channels, {args.domains} domains"}[mode]
     parallelism = {"image": f"image-sharded x{world} (no collective)",
                    "jungfrau": f"image-sharded x{world} (no collective)",
-                   "channels": f"channel-sharded x{world}, FP64 partials reduced to rank 0 (NCCL), finalize on rank 0"}
+                   "channels": (f"channel-sharded x{world}, FP64 partials stored by each rank's kernel into rank 0's "
+                                f"peer-memory slots, summed on rank 0" if args.transport == "p2p" and world > 1 else
+                                f"channel-sharded x{world}, FP64 partials reduced to rank 0 (NCCL), finalize on rank 0")}
     result = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,
@@ -313,7 +339,7 @@ def run_ours(args):
 
         def e2e_call(c):
             if mode == "channels":
-                parallel.simulate_channel_sharded(c, img)
+                parallel.simulate_channel_sharded(c, img, transport=args.transport)
             else:
                 nanobragg_spots(c, img)
 

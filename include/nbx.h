@@ -56,7 +56,9 @@ enum {
     NBX_OUT_IMAGE_F64 = 4, /* out[p] = f64(f32(spots)) + f64(f32(background)): the simulate_image
                               accumulator (scheduler.py:156-183) in one launch; background only when
                               the descriptor carries a profile (bg_points > 0) */
-    NBX_OUT_IMAGE_F32 = 5  /* out[p] = f32(IMAGE_F64 value): the write_image payload (io.py:403-434) */
+    NBX_OUT_IMAGE_F32 = 5, /* out[p] = f32(IMAGE_F64 value): the write_image payload (io.py:403-434) */
+    NBX_OUT_RAW_STORE_F64 = 6 /* out[p] = acc (unscaled partial, plain store): a channel shard written
+                                 straight into the root's slot over peer memory (nbx_ipc_*) */
 };
 
 /* Lattice shape transforms.  SINCG is the reference's grating
@@ -223,6 +225,20 @@ int nbx_background(void* ctx, const nbx_spots_desc* d, int out_mode, void* out, 
  * SURVEY §8 E1): out = mode(scale * raw).  raw is a device pointer. */
 int nbx_finalize(void* ctx, const double* raw, int64_t n, double scale, int out_mode,
                  void* out, int out_on_device, int64_t* first_bad);
+
+/* Fused channel-shard transport over peer memory, the alternative
+ * to a separate NCCL reduce: the root allocates one FP64 slot per rank in IPC-shareable
+ * memory (nbx_ipc_alloc), every other rank maps it (nbx_ipc_open) and its spot kernel's
+ * epilogue stores its partial straight into its slot (NBX_OUT_RAW_STORE_F64) -- the transfer
+ * happens pixel by pixel while the image is computed -- and after a barrier the root sums
+ * the slots in rank order, scales and stores (nbx_reduce_slots).  handle is 64 bytes. */
+int nbx_ipc_alloc(void* ctx, int64_t bytes, void** dev, unsigned char* handle);
+int nbx_ipc_free(void* ctx, void* dev);
+int nbx_ipc_open(void* ctx, const unsigned char* handle, void** dev);
+int nbx_ipc_close(void* ctx, void* dev);
+/* out = mode(scale * sum_{r < n_slots} slots[r*n + p]), summed in rank order (deterministic). */
+int nbx_reduce_slots(void* ctx, const double* slots, int n_slots, int64_t n, double scale, int out_mode,
+                     void* out, int out_on_device, int64_t* first_bad);
 
 /* lhs[j] += (double) rhs[j] -- add_array (kernels.py:315-331). */
 int nbx_add_array(void* ctx, double* lhs, const float* rhs, int64_t n, int on_device);

@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("NBX_LIB") or Path(__file__).resolve().parent / "
 
 NBX_OK, NBX_ERR_ARG, NBX_ERR_NUMERICAL, NBX_ERR_CUDA = 0, 1, 2, 3
 COMPUTE = {"fp64": 0, "fp32": 1}
-OUT_F32, OUT_F64, OUT_ADD_F64, OUT_RAW_F64, OUT_IMAGE_F64, OUT_IMAGE_F32 = 0, 1, 2, 3, 4, 5
+OUT_F32, OUT_F64, OUT_ADD_F64, OUT_RAW_F64, OUT_IMAGE_F64, OUT_IMAGE_F32, OUT_RAW_STORE_F64 = 0, 1, 2, 3, 4, 5, 6
 SHAPES = {"sincg": 0, "square": 0, "gauss": 1, "round": 2, "tophat": 3}
 
 # Every exported symbol of include/nbx.h (checked by tests/test_abi.py).
@@ -29,7 +29,7 @@ EXPORTS = (
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
     "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak", "nbx_background",
     "nbx_fault_stage", "nbx_campaign", "nbx_crc32", "nbx_image_stats", "nbx_image_histogram",
-    "nbx_struct_size",
+    "nbx_struct_size", "nbx_ipc_alloc", "nbx_ipc_free", "nbx_ipc_open", "nbx_ipc_close", "nbx_reduce_slots",
 )
 
 
@@ -111,6 +111,11 @@ def load() -> C.CDLL:
             "nbx_image_histogram": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                               C.c_double, i64p, i64p, i64p]),
             "nbx_struct_size": (C.c_int64, [C.c_int]),
+            "nbx_ipc_alloc": (C.c_int, [vp, C.c_int64, C.POINTER(vp), C.c_char_p]),
+            "nbx_ipc_free": (C.c_int, [vp, vp]),
+            "nbx_ipc_open": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+            "nbx_ipc_close": (C.c_int, [vp, vp]),
+            "nbx_reduce_slots": (C.c_int, [vp, vp, C.c_int, C.c_int64, C.c_double, C.c_int, vp, C.c_int, i64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

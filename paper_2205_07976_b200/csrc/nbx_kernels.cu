@@ -28,7 +28,8 @@
 
 namespace nbx {
 
-enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 4, kOutImageF32 = 5 };
+enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 4, kOutImageF32 = 5,
+       kOutRawStoreF64 = 6 };
 
 // ---------------------------------------------------------------------------
 // Diffuse background of one pixel (kernels.py:279-312): pixel-centre geometry
@@ -580,6 +581,10 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
             static_cast<double*>(P.out)[p] += acc * P.raw_scale;
             break;
         }
+        case kOutRawStoreF64: {  // the same partial stored into the root's slot (peer memory)
+            static_cast<double*>(P.out)[p] = acc * P.raw_scale;
+            break;
+        }
         default: {  // kOutImageF64/F32: simulate_image's accumulator, spots (+ background) fused
             const float v = (float)(P.out_scale * acc);
             bad = !isfinite(v);
@@ -632,6 +637,30 @@ __global__ void finalize_kernel(const double* __restrict__ raw, int64_t n, doubl
                                 unsigned long long* fault) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const double acc = raw[p];
+        bool bad;
+        if (mode == kOutF32) {
+            const float v = (float)(scale * acc);
+            static_cast<float*>(out)[p] = v;
+            bad = !isfinite(v);
+        } else if (mode == kOutF64) {
+            const double v = scale * acc;
+            static_cast<double*>(out)[p] = v;
+            bad = !isfinite(v);
+        } else {
+            const float v = (float)(scale * acc);
+            static_cast<double*>(out)[p] += (double)v;
+            bad = !isfinite(v);
+        }
+        if (bad) atomicMin(fault, (unsigned long long)p);
+    }
+}
+
+// Root of a peer-memory channel-sharded image: sum the ranks' slots in rank order, scale, store.
+__global__ void reduce_slots_kernel(const double* __restrict__ slots, int n_slots, int64_t n, double scale, int mode,
+                                    void* out, unsigned long long* fault) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < n_slots; ++r) acc += slots[(int64_t)r * n + p];
         bool bad;
         if (mode == kOutF32) {
             const float v = (float)(scale * acc);
@@ -723,6 +752,12 @@ cudaError_t launch_background(const SpotsParams& P, cudaStream_t st) {
 cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
                             unsigned long long* fault, cudaStream_t st) {
     finalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(raw, n, scale, mode, out, fault);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_slots(const double* slots, int n_slots, int64_t n, double scale, int mode, void* out,
+                                unsigned long long* fault, cudaStream_t st) {
+    reduce_slots_kernel<<<grid_for(n, 256), 256, 0, st>>>(slots, n_slots, n, scale, mode, out, fault);
     return cudaGetLastError();
 }
 

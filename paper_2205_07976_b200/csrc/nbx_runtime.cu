@@ -24,6 +24,8 @@
 
 namespace nbx {
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
+cudaError_t launch_reduce_slots(const double* slots, int n_slots, int64_t n, double scale, int mode, void* out,
+                                unsigned long long* fault, cudaStream_t st);
 cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
                             unsigned long long* fault, cudaStream_t st);
 cudaError_t launch_add_array(double* lhs, const float* rhs, int64_t n, cudaStream_t st);
@@ -815,7 +817,7 @@ size_t out_elem_bytes(int mode) {
 }
 
 void check_mode(int mode) {
-    if (mode < NBX_OUT_F32 || mode > NBX_OUT_IMAGE_F32) throw ArgError("unknown output mode");
+    if (mode < NBX_OUT_F32 || mode > NBX_OUT_RAW_STORE_F64) throw ArgError("unknown output mode");
 }
 
 // Three fault slots per launch: spots, background, f32 downcast of the image.
@@ -1181,9 +1183,15 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
                     for (int i = 0; i < d->n_sources; ++i) wsum += d->weights[i];
                     sh.norm = wsum * (double)d->n_domains * (double)(d->oversample * d->oversample);
                 }
-                const bool raw_out = out_mode == NBX_OUT_RAW_F64;
+                const bool raw_out = out_mode == NBX_OUT_RAW_F64 || out_mode == NBX_OUT_RAW_STORE_F64;
                 void* acc = out;
                 int acc_on_device = out_on_device;
+                if (out_mode == NBX_OUT_RAW_STORE_F64) {  // store semantics: start from zero
+                    if (out_on_device)
+                        NBX_CUDA(cudaMemsetAsync(out, 0, (size_t)npix * sizeof(double), ctx->stream));
+                    else
+                        std::memset(out, 0, (size_t)npix * sizeof(double));
+                }
                 if (!raw_out) {
                     ctx->raw_scratch.ensure((size_t)npix * sizeof(double));
                     NBX_CUDA(cudaMemsetAsync(ctx->raw_scratch.p, 0, (size_t)npix * sizeof(double), ctx->stream));
@@ -1200,7 +1208,7 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
                 }
                 return NBX_OK;
             });
-            if (st != NBX_OK || out_mode == NBX_OUT_RAW_F64) return st;
+            if (st != NBX_OK || out_mode == NBX_OUT_RAW_F64 || out_mode == NBX_OUT_RAW_STORE_F64) return st;
             return nbx_finalize(ctxp, static_cast<const double*>(static_cast<Ctx*>(ctxp)->raw_scratch.p), npix, scale,
                                 out_mode, out, out_on_device, first_bad);
         }
@@ -1499,6 +1507,80 @@ int nbx_finalize(void* ctxp, const double* raw, int64_t n, double scale, int out
         ctx->fault.ensure(8);
         NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 8, s));
         NBX_CUDA(nbx::launch_finalize(raw, n, scale, out_mode, dout, static_cast<unsigned long long*>(ctx->fault.p), s));
+        unsigned long long f = ~0ull;
+        NBX_CUDA(cudaMemcpyAsync(&f, ctx->fault.p, 8, cudaMemcpyDeviceToHost, s));
+        if (!out_on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+        NBX_CUDA(cudaStreamSynchronize(s));
+        bad = f == ~0ull ? -1 : (int64_t)f;
+        return NBX_OK;
+    });
+    if (st != NBX_OK) return st;
+    return fault_status(ctxp, bad, first_bad);
+}
+
+int nbx_ipc_alloc(void* ctxp, int64_t bytes, void** dev, unsigned char* handle) {
+    return guarded(ctxp, [&] {
+        if (!ctxp || !dev || !handle || bytes <= 0) throw ArgError("invalid ipc_alloc arguments");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        NBX_CUDA(cudaMalloc(dev, (size_t)bytes));
+        cudaIpcMemHandle_t h;
+        NBX_CUDA(cudaIpcGetMemHandle(&h, *dev));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(handle, &h, sizeof(h));
+        return NBX_OK;
+    });
+}
+
+int nbx_ipc_free(void* ctxp, void* dev) {
+    return guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        if (dev) NBX_CUDA(cudaFree(dev));
+        return NBX_OK;
+    });
+}
+
+int nbx_ipc_open(void* ctxp, const unsigned char* handle, void** dev) {
+    return guarded(ctxp, [&] {
+        if (!ctxp || !handle || !dev) throw ArgError("invalid ipc_open arguments");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        NBX_CUDA(cudaIpcOpenMemHandle(dev, h, cudaIpcMemLazyEnablePeerAccess));
+        return NBX_OK;
+    });
+}
+
+int nbx_ipc_close(void* ctxp, void* dev) {
+    return guarded(ctxp, [&] {
+        if (!ctxp) throw ArgError("NULL context");
+        NBX_CUDA(cudaSetDevice(static_cast<Ctx*>(ctxp)->device));
+        if (dev) NBX_CUDA(cudaIpcCloseMemHandle(dev));
+        return NBX_OK;
+    });
+}
+
+int nbx_reduce_slots(void* ctxp, const double* slots, int n_slots, int64_t n, double scale, int out_mode, void* out,
+                     int out_on_device, int64_t* first_bad) {
+    int64_t bad = -1;
+    int st = guarded(ctxp, [&] {
+        if (!ctxp || !slots || !out || n_slots < 1 || n < 0) throw ArgError("invalid reduce_slots arguments");
+        if (out_mode != NBX_OUT_F32 && out_mode != NBX_OUT_F64 && out_mode != NBX_OUT_ADD_F64)
+            throw ArgError("reduce_slots output mode must be F32, F64 or ADD_F64");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const size_t bytes = (size_t)n * out_elem_bytes(out_mode);
+        void* dout = out;
+        if (!out_on_device) {
+            ctx->out_scratch.ensure(bytes);
+            dout = ctx->out_scratch.p;
+            if (out_mode == NBX_OUT_ADD_F64) NBX_CUDA(cudaMemcpyAsync(dout, out, bytes, cudaMemcpyHostToDevice, s));
+        }
+        ctx->fault.ensure(8);
+        NBX_CUDA(cudaMemsetAsync(ctx->fault.p, 0xFF, 8, s));
+        NBX_CUDA(nbx::launch_reduce_slots(slots, n_slots, n, scale, out_mode, dout,
+                                          static_cast<unsigned long long*>(ctx->fault.p), s));
         unsigned long long f = ~0ull;
         NBX_CUDA(cudaMemcpyAsync(&f, ctx->fault.p, 8, cudaMemcpyDeviceToHost, s));
         if (!out_on_device) NBX_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));

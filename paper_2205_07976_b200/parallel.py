@@ -84,17 +84,72 @@ def _gpu_finalize(raw, scale: float, out: PixelBuffer):
     N.check(cx, status, bad.value)
 
 
+def _p2p_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None, group, root: int, world: int, rank: int):
+    """Fused transport: every rank's spot kernel stores its FP64 partial straight into its slot of
+    an IPC-shared buffer on the root (NBX_OUT_RAW_STORE_F64 epilogue, the transfer overlapping
+    the computation pixel by pixel); after a barrier the root sums the slots in rank order."""
+    import torch
+    import torch.distributed as dist
+
+    cx = N.context()
+    lo, hi = channel_shards(len(ctx.spectrum.samples), world)[rank]
+    plan = SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=global_norm(ctx), device=torch.cuda.current_device())
+    npix = plan.n_pixels
+    base = N.C.c_void_p()
+    handle = [None]
+    if rank == root:
+        buf = N.C.create_string_buffer(64)
+        N.check(cx, cx.lib.nbx_ipc_alloc(cx.handle, world * npix * 8, N.C.byref(base), buf))
+        handle = [bytes(buf.raw)]
+    dist.broadcast_object_list(handle, src=root, group=group)
+    if rank != root:
+        N.check(cx, cx.lib.nbx_ipc_open(cx.handle, handle[0], N.C.byref(base)))
+    try:
+        slot = base.value + rank * npix * 8
+        torch.cuda.synchronize()
+        plan.run(slot, mode=N.OUT_RAW_STORE_F64, on_device=True)  # synchronous: our stores are done
+        scale = plan.scale
+        dist.barrier(group=group)  # every rank's slot is written
+        result = None
+        if rank == root:
+            result = out if out is not None else PixelBuffer.zeros(ctx.panel.dims, "f32")
+            mode = N.OUT_F32 if result.precision == "f32" else N.OUT_F64
+            bad = N.C.c_int64(-1)
+            st = cx.lib.nbx_reduce_slots(cx.handle, base.value, world, npix, scale, mode, result.data.ctypes.data, 0,
+                                         N.C.byref(bad))
+            N.check(cx, st, bad.value)
+        dist.barrier(group=group)  # the root has read every slot
+    finally:
+        plan.close()
+        if rank == root:
+            cx.lib.nbx_ipc_free(cx.handle, base)
+        else:
+            cx.lib.nbx_ipc_close(cx.handle, base)
+    return result
+
+
 def simulate_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None = None, *, group=None, root: int = 0,
-                             partial: Callable | None = None, finalize: Callable | None = None):
+                             partial: Callable | None = None, finalize: Callable | None = None,
+                             transport: str = "nccl"):
     """One image split by energy channel over the ranks of ``group``; returns the image on root, else None.
 
-    ``partial(ctx, lo, hi, norm) -> (raw_tensor, scale)`` and
-    ``finalize(raw_tensor, scale, out)`` default to the GPU library.
+    ``transport="nccl"`` (default, the north star's NCCL reduce): partial images in CUDA
+    tensors, one ``dist.reduce`` to the root, scale + store there.  ``transport="p2p"``: the
+    partials are stored by each rank's kernel directly into the root's memory (CUDA IPC /
+    NVLink peer stores) and summed there in rank order -- no separate collective.
+    ``partial(ctx, lo, hi, norm) -> (raw_tensor, scale)`` and ``finalize(raw_tensor, scale,
+    out)`` (NCCL transport) default to the GPU library.
     """
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if transport == "p2p" and world > 1:
+        if len(ctx.spectrum.samples) < world:
+            raise ValueError(f"{len(ctx.spectrum.samples)} sources cannot be split over {world} ranks")
+        return _p2p_channel_sharded(ctx, out, group, root, world, rank)
+    if transport not in ("nccl", "p2p"):
+        raise ValueError("transport must be 'nccl' or 'p2p'")
     partial = partial or _gpu_partial
     finalize = finalize or _gpu_finalize
     n_src = len(ctx.spectrum.samples)

@@ -34,8 +34,10 @@ def test_image_sharded_two_ranks(gpu):
     assert d["value"] > 0 and d["gpu_launches"] == 2
 
 
-def test_channel_sharded_two_ranks(gpu):
-    d = torchrun(["--mode", "channels", "--channels", "64", "--steps", "2", "--warmup", "3", "--size", "512"], 29532)
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_channel_sharded_two_ranks(gpu, transport):
+    d = torchrun(["--mode", "channels", "--channels", "64", "--steps", "2", "--warmup", "3", "--size", "512",
+                  "--transport", transport], 29532 if transport == "nccl" else 29536)
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["images_per_gpu_per_step"] == 0.5
     assert d["value"] > 0 and d["e2e"]["value"] > 0
 
@@ -75,3 +77,46 @@ def test_campaign_sharded_over_two_ranks(gpu, tmp_path):
     assert one.returncode == 0, one.stderr[-3000:]
     r1 = json.loads([ln for ln in one.stdout.splitlines() if ln.startswith("{")][0])
     assert dict(zip(r1["indices"], r1["crcs"])) == crc2
+
+
+P2P_SCRIPT = r'''
+import os, sys, json
+sys.path.insert(0, os.environ["NBX_ROOT"])
+import numpy as np
+import torch, torch.distributed as dist
+from paper_2205_07976_b200 import PixelBuffer, nanobragg_spots, parallel, synthetic
+dist.init_process_group("gloo")
+torch.cuda.set_device(0)
+panel = synthetic.roi(synthetic.rayonix_panel(), 1880, 1880, 40, 48)
+res = {}
+for compute in ("fp64", "fp32"):
+    ctx = synthetic.ls49_context(panel=panel, n_channels=9, n_domains=3, compute=compute)
+    a = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(panel.dims, "f64"), transport="p2p")
+    b = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(panel.dims, "f64"), transport="nccl")
+    if dist.get_rank() == 0:
+        whole = PixelBuffer.zeros(panel.dims, "f64")
+        nanobragg_spots(ctx, whole)
+        res[compute] = {"p2p_vs_reduce": float(np.abs(a.data - b.data).max() / np.abs(b.data).max()),
+                        "p2p_vs_whole": float(np.abs(a.data - whole.data).max() / np.abs(whole.data).max())}
+    else:
+        assert a is None and b is None
+if dist.get_rank() == 0:
+    print(json.dumps(res), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_p2p_channel_sharded_transport_two_ranks(gpu, tmp_path):
+    """The fused peer-memory transport for channel shards (each rank's kernel stores its partial
+    into the root's IPC-mapped slot; the root sums slots in rank order) equals the reduce-based
+    path and the whole image (both ranks on one GPU here; NVLink peers on a real box)."""
+    script = tmp_path / "p2p.py"
+    script.write_text(P2P_SCRIPT)
+    env = dict(os.environ, NBX_ROOT=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29535", str(script)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    d = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["fp64"]["p2p_vs_reduce"] < 1e-15 and d["fp64"]["p2p_vs_whole"] < 1e-12, d
+    assert d["fp32"]["p2p_vs_reduce"] < 1e-15 and d["fp32"]["p2p_vs_whole"] < 1e-4, d
