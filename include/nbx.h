@@ -150,6 +150,9 @@ int nbx_version(void);
  * mirrors: 0 nbx_panel, 1 nbx_spots_desc, 2 nbx_plan_info_t (0 for anything else). */
 int64_t nbx_struct_size(int which);
 
+/* Number of CUDA devices visible to this process (0 without a GPU or driver). */
+int nbx_device_count(void);
+
 /* Per-device context: stream, scratch, last error.  NULL on failure (no GPU). */
 void* nbx_ctx_create(int device);
 void nbx_ctx_destroy(void* ctx);

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 from pathlib import Path
 
@@ -29,7 +30,7 @@ EXPORTS = (
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
     "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak", "nbx_background",
     "nbx_fault_stage", "nbx_campaign", "nbx_crc32", "nbx_image_stats", "nbx_image_histogram",
-    "nbx_struct_size", "nbx_ipc_alloc", "nbx_ipc_free", "nbx_ipc_open", "nbx_ipc_close", "nbx_reduce_slots",
+    "nbx_struct_size", "nbx_device_count", "nbx_ipc_alloc", "nbx_ipc_free", "nbx_ipc_open", "nbx_ipc_close", "nbx_reduce_slots",
 )
 
 
@@ -111,6 +112,7 @@ def load() -> C.CDLL:
             "nbx_image_histogram": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double,
                                               C.c_double, i64p, i64p, i64p]),
             "nbx_struct_size": (C.c_int64, [C.c_int]),
+            "nbx_device_count": (C.c_int, []),
             "nbx_ipc_alloc": (C.c_int, [vp, C.c_int64, C.POINTER(vp), C.c_char_p]),
             "nbx_ipc_free": (C.c_int, [vp, vp]),
             "nbx_ipc_open": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
@@ -126,7 +128,20 @@ def load() -> C.CDLL:
 
 
 def default_device() -> int:
-    return int(os.environ.get("NBX_DEVICE", "0"))
+    """Device of the default context: NBX_DEVICE if set; else torch's current device once torch
+    has initialised CUDA (``torch.cuda.set_device(local_rank)``); else LOCAL_RANK under torchrun
+    (one process per GPU, wrapped onto the visible devices); else 0."""
+    env = os.environ.get("NBX_DEVICE")
+    if env is not None:
+        return int(env)
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        return int(torch.cuda.current_device())
+    local = os.environ.get("LOCAL_RANK")
+    if local is not None:
+        n = load().nbx_device_count()
+        return int(local) % n if n > 0 else 0
+    return 0
 
 
 class Context:
@@ -134,6 +149,10 @@ class Context:
 
     def __init__(self, device: int | None = None):
         self.lib = load()
+        # The C ABI serves one host thread at a time per context (include/nbx.h); ctypes drops
+        # the GIL during calls, so every call that touches this context's streams / scratch and
+        # the status check that reads its last-error string happen under this lock.
+        self.lock = threading.RLock()
         self.device = default_device() if device is None else int(device)
         self.handle = self.lib.nbx_ctx_create(self.device)
         if not self.handle:

@@ -55,7 +55,6 @@ struct CudaError : std::runtime_error {
             throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));               \
     } while (0)
 
-// Device buffer that frees itself.
 // Pinned host staging buffer (grown, never shrunk) for table uploads.
 struct HostBuf {
     void* p = nullptr;
@@ -80,6 +79,7 @@ struct HostBuf {
     }
 };
 
+// Device buffer that frees itself (grown, never shrunk).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -1019,6 +1019,15 @@ int64_t nbx_struct_size(int which) {
         case 2: return (int64_t)sizeof(nbx_plan_info_t);
         default: return 0;
     }
+}
+
+int nbx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 void* nbx_ctx_create(int device) {

@@ -28,7 +28,7 @@ from typing import Callable, NamedTuple
 import numpy as np
 
 from . import _native as N
-from .errors import NumericalFault, PatternFault
+from .errors import NumericalFault, PatternFault, ShapeMismatchError
 from .kernels import PixelBuffer, describe
 
 __all__ = ["write_image", "read_image", "run_campaign", "CampaignResult", "image_stats", "image_histogram",
@@ -143,17 +143,22 @@ def run_campaign(context_for: Callable[[int], object], n_images: int, out_dir, *
     bad = C.c_int64(-1)
     compute = N.COMPUTE[getattr(ctxs[0], "compute", "fp64")] if ctxs else 0
     t0 = time.perf_counter()
-    status = cx.lib.nbx_campaign(cx.handle, arr, n, compute, cpaths, crcs, C.byref(bad))
+    with cx.lock:
+        status = cx.lib.nbx_campaign(cx.handle, arr, n, compute, cpaths, crcs, C.byref(bad))
+        stage = cx.lib.nbx_fault_stage(cx.handle)
+        msg = cx.error() if status not in (N.NBX_OK, N.NBX_ERR_NUMERICAL) else ""
     seconds = time.perf_counter() - t0
     if status == N.NBX_ERR_NUMERICAL:
         img, pix = bad.value >> 40, bad.value & ((1 << 40) - 1)
-        stage = cx.lib.nbx_fault_stage(cx.handle)
         cause = NumericalFault(pix)
         if stage == 2:  # write_image refuses the non-finite downcast (io.py:409-411)
             raise NumericalFault(pix, f"image {indices[img]}: refusing to write non-finite pixel {pix}")
         label = "nanobragg_spots" if stage == 0 else "add_background"
         raise PatternFault(label, pix, cause) from cause
-    N.check(cx, status, label="run_campaign")
+    if status != N.NBX_OK:
+        if status == N.NBX_ERR_ARG:
+            raise ShapeMismatchError(msg) if "dims" in msg or "buffer" in msg else ValueError(msg)
+        raise N.NativeError(msg)
     for i, (stem, c, crc) in enumerate(zip(stems, ctxs, crcs)):
         _write_sidecar(stem, _sidecar(c.panel.dims, crc, c.panel, c.spectrum,
                                       seeds(indices[i]) if seeds else None, indices[i]))
@@ -190,8 +195,9 @@ def image_stats(buf: PixelBuffer, executor=None) -> ImageStats:
     cx = N.context()
     out = (C.c_double * 4)()
     data = np.ascontiguousarray(buf.data)
-    status = cx.lib.nbx_image_stats(cx.handle, data.ctypes.data, data.size, _dtype_code(buf), 0, out)
-    N.check(cx, status, label="image_stats")
+    with cx.lock:
+        status = cx.lib.nbx_image_stats(cx.handle, data.ctypes.data, data.size, _dtype_code(buf), 0, out)
+        N.check(cx, status, label="image_stats")
     return ImageStats(out[0], out[1], out[2], out[3])
 
 
@@ -209,8 +215,9 @@ def image_histogram(buf: PixelBuffer, n_bins: int, value_range: tuple[float, flo
     counts = np.zeros(n_bins, dtype=np.int64)
     under, over = C.c_int64(0), C.c_int64(0)
     data = np.ascontiguousarray(buf.data)
-    status = cx.lib.nbx_image_histogram(cx.handle, data.ctypes.data, data.size, _dtype_code(buf), 0, n_bins, lo,
-                                        hi, counts.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(under),
-                                        C.byref(over))
-    N.check(cx, status, label="image_histogram")
+    with cx.lock:
+        status = cx.lib.nbx_image_histogram(cx.handle, data.ctypes.data, data.size, _dtype_code(buf), 0, n_bins,
+                                            lo, hi, counts.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(under),
+                                            C.byref(over))
+        N.check(cx, status, label="image_histogram")
     return HistogramResult(counts, np.cumsum(counts), int(under.value), int(over.value))

@@ -210,9 +210,10 @@ def nanobragg_spots(ctx: SpotsContext, out: PixelBuffer, executor=None) -> None:
     mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
     bad = N.C.c_int64(-1)
     compute = N.COMPUTE[getattr(ctx, "compute", "fp64")]
-    status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), compute, mode,
-                              out.data.ctypes.data, 0, N.C.byref(bad))
-    N.check(cx, status, bad.value)
+    with cx.lock:
+        status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), compute, mode,
+                                  out.data.ctypes.data, 0, N.C.byref(bad))
+        N.check(cx, status, bad.value)
     if executor is not None and hasattr(executor, "timing_log"):
         from .execution import TimingRecord
 
@@ -231,11 +232,13 @@ class SpotsPlan:
                  src_end: int = 0, norm: float = 0.0):
         self.cx = N.context(device)
         self.desc = describe(ctx, src_begin=src_begin, src_end=src_end, norm=norm)
-        self.handle = self.cx.lib.nbx_plan_create(self.cx.handle, N.C.byref(self.desc.c), N.COMPUTE[ctx.compute])
-        if not self.handle:
-            N.check(self.cx, N.NBX_ERR_ARG if "cuda" not in self.cx.error().lower() else N.NBX_ERR_CUDA)
-        info = N.PlanInfo()
-        self.cx.lib.nbx_plan_info(self.handle, N.C.byref(info))
+        with self.cx.lock:
+            self.handle = self.cx.lib.nbx_plan_create(self.cx.handle, N.C.byref(self.desc.c),
+                                                      N.COMPUTE[ctx.compute])
+            if not self.handle:
+                N.check(self.cx, N.NBX_ERR_ARG if "cuda" not in self.cx.error().lower() else N.NBX_ERR_CUDA)
+            info = N.PlanInfo()
+            self.cx.lib.nbx_plan_info(self.handle, N.C.byref(info))
         self.info = info
         self.dims = _dims_of(ctx.panel)
 
@@ -263,8 +266,9 @@ class SpotsPlan:
         else:
             addr, dev = int(out), 1 if on_device else 0
         bad = N.C.c_int64(-1)
-        status = self.cx.lib.nbx_plan_run(self.handle, mode, addr, dev, N.C.byref(bad))
-        N.check(self.cx, status, bad.value)
+        with self.cx.lock:
+            status = self.cx.lib.nbx_plan_run(self.handle, mode, addr, dev, N.C.byref(bad))
+            N.check(self.cx, status, bad.value)
 
     @property
     def kernel_ms(self) -> float:
@@ -272,8 +276,9 @@ class SpotsPlan:
 
     def close(self):
         if getattr(self, "handle", None):
-            self.cx.lib.nbx_plan_destroy(self.handle)
-            self.handle = None
+            with self.cx.lock:
+                self.cx.lib.nbx_plan_destroy(self.handle)
+                self.handle = None
 
     def __del__(self):
         try:
@@ -304,8 +309,10 @@ def add_background(profile, panel, spectrum, thickness_factor: float, out: Pixel
     cx = N.context()
     bad = N.C.c_int64(-1)
     mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
-    status = cx.lib.nbx_background(cx.handle, N.C.byref(desc.c), mode, out.data.ctypes.data, 0, N.C.byref(bad))
-    N.check(cx, status, bad.value, label="add_background")
+    with cx.lock:
+        status = cx.lib.nbx_background(cx.handle, N.C.byref(desc.c), mode, out.data.ctypes.data, 0,
+                                       N.C.byref(bad))
+        N.check(cx, status, bad.value, label="add_background")
     if executor is not None and hasattr(executor, "timing_log"):
         from .execution import TimingRecord
 
@@ -331,9 +338,10 @@ def simulate_image(ctx, background=None, thickness_factor: float = 1.0, out: Pix
     desc = describe(ctx, background=background, thickness_factor=thickness_factor)
     cx = N.context()
     bad = N.C.c_int64(-1)
-    status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), N.COMPUTE[getattr(ctx, "compute", "fp64")],
-                              N.OUT_IMAGE_F64, out.data.ctypes.data, 0, N.C.byref(bad))
-    N.check(cx, status, bad.value, label="simulate_image")
+    with cx.lock:
+        status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), N.COMPUTE[getattr(ctx, "compute", "fp64")],
+                                  N.OUT_IMAGE_F64, out.data.ctypes.data, 0, N.C.byref(bad))
+        N.check(cx, status, bad.value, label="simulate_image")
     if executor is not None and hasattr(executor, "timing_log"):
         from .execution import TimingRecord
 
@@ -349,8 +357,9 @@ def add_array(lhs: PixelBuffer, rhs: PixelBuffer, executor=None) -> None:
         raise ShapeMismatchError("add_array expects f64 lhs and f32 rhs")
     cx = N.context()
     rhs_data = np.ascontiguousarray(rhs.data)
-    status = cx.lib.nbx_add_array(cx.handle, lhs.data.ctypes.data, rhs_data.ctypes.data, lhs.n_pixels, 0)
-    N.check(cx, status, label="add_array")
+    with cx.lock:
+        status = cx.lib.nbx_add_array(cx.handle, lhs.data.ctypes.data, rhs_data.ctypes.data, lhs.n_pixels, 0)
+        N.check(cx, status, label="add_array")
 
 
 def add_noise(buf: PixelBuffer, seed: int, image: int = 0) -> PixelBuffer:
@@ -363,9 +372,10 @@ def add_noise(buf: PixelBuffer, seed: int, image: int = 0) -> PixelBuffer:
     out = PixelBuffer(buf.dims, buf.precision)
     dtype = 0 if buf.precision == "f32" else 1
     src = np.ascontiguousarray(buf.data)
-    status = cx.lib.nbx_add_noise(cx.handle, src.ctypes.data, out.data.ctypes.data, buf.n_pixels, dtype,
-                                  int(seed) & (2**64 - 1), int(image) & (2**64 - 1), 0)
-    N.check(cx, status, label="add_noise")
+    with cx.lock:
+        status = cx.lib.nbx_add_noise(cx.handle, src.ctypes.data, out.data.ctypes.data, buf.n_pixels, dtype,
+                                      int(seed) & (2**64 - 1), int(image) & (2**64 - 1), 0)
+        N.check(cx, status, label="add_noise")
     return out
 
 

@@ -76,12 +76,13 @@ def _gpu_partial(ctx: SpotsContext, lo: int, hi: int, norm: float):
 
 
 def _gpu_finalize(raw, scale: float, out: PixelBuffer):
-    cx = N.context()
+    cx = N.context(raw.device.index)
     mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
     bad = N.C.c_int64(-1)
-    status = cx.lib.nbx_finalize(cx.handle, raw.data_ptr(), raw.numel(), scale, mode, out.data.ctypes.data, 0,
-                                 N.C.byref(bad))
-    N.check(cx, status, bad.value)
+    with cx.lock:
+        status = cx.lib.nbx_finalize(cx.handle, raw.data_ptr(), raw.numel(), scale, mode, out.data.ctypes.data, 0,
+                                     N.C.byref(bad))
+        N.check(cx, status, bad.value)
 
 
 def _p2p_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None, group, root: int, world: int, rank: int):
@@ -91,19 +92,22 @@ def _p2p_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None, group, root
     import torch
     import torch.distributed as dist
 
-    cx = N.context()
+    dev = torch.cuda.current_device()
+    cx = N.context(dev)
     lo, hi = channel_shards(len(ctx.spectrum.samples), world)[rank]
-    plan = SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=global_norm(ctx), device=torch.cuda.current_device())
+    plan = SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=global_norm(ctx), device=dev)
     npix = plan.n_pixels
     base = N.C.c_void_p()
     handle = [None]
     if rank == root:
         buf = N.C.create_string_buffer(64)
-        N.check(cx, cx.lib.nbx_ipc_alloc(cx.handle, world * npix * 8, N.C.byref(base), buf))
+        with cx.lock:
+            N.check(cx, cx.lib.nbx_ipc_alloc(cx.handle, world * npix * 8, N.C.byref(base), buf))
         handle = [bytes(buf.raw)]
     dist.broadcast_object_list(handle, src=root, group=group)
     if rank != root:
-        N.check(cx, cx.lib.nbx_ipc_open(cx.handle, handle[0], N.C.byref(base)))
+        with cx.lock:
+            N.check(cx, cx.lib.nbx_ipc_open(cx.handle, handle[0], N.C.byref(base)))
     try:
         slot = base.value + rank * npix * 8
         torch.cuda.synchronize()
@@ -115,16 +119,18 @@ def _p2p_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None, group, root
             result = out if out is not None else PixelBuffer.zeros(ctx.panel.dims, "f32")
             mode = N.OUT_F32 if result.precision == "f32" else N.OUT_F64
             bad = N.C.c_int64(-1)
-            st = cx.lib.nbx_reduce_slots(cx.handle, base.value, world, npix, scale, mode, result.data.ctypes.data, 0,
-                                         N.C.byref(bad))
-            N.check(cx, st, bad.value)
+            with cx.lock:
+                st = cx.lib.nbx_reduce_slots(cx.handle, base.value, world, npix, scale, mode,
+                                             result.data.ctypes.data, 0, N.C.byref(bad))
+                N.check(cx, st, bad.value)
         dist.barrier(group=group)  # the root has read every slot
     finally:
         plan.close()
-        if rank == root:
-            cx.lib.nbx_ipc_free(cx.handle, base)
-        else:
-            cx.lib.nbx_ipc_close(cx.handle, base)
+        with cx.lock:
+            if rank == root:
+                cx.lib.nbx_ipc_free(cx.handle, base)
+            else:
+                cx.lib.nbx_ipc_close(cx.handle, base)
     return result
 
 

@@ -129,3 +129,17 @@ def test_integration_doc_binding_matches_the_library(lib):
     assert lib.nbx_struct_size(0) == C.sizeof(ns["Panel"])
     assert lib.nbx_struct_size(1) == C.sizeof(ns["Desc"])
     assert [f[0] for f in ns["Desc"]._fields_] == [f[0] for f in _native.SpotsDesc._fields_]
+
+
+def test_default_device_follows_nbx_device_then_local_rank(monkeypatch):
+    """The default context's device: NBX_DEVICE wins; under torchrun LOCAL_RANK wrapped onto the
+    visible devices (0 here: no GPU in this container, nbx_device_count() == 0)."""
+    monkeypatch.setenv("NBX_DEVICE", "3")
+    assert _native.default_device() == 3
+    monkeypatch.delenv("NBX_DEVICE")
+    monkeypatch.setenv("LOCAL_RANK", "5")
+    n = _native.load().nbx_device_count()
+    assert n >= 0
+    torch = __import__("sys").modules.get("torch")
+    if torch is None or not torch.cuda.is_initialized():
+        assert _native.default_device() == (5 % n if n else 0)

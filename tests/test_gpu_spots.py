@@ -573,3 +573,27 @@ def test_batch_api_equals_single_images(gpu):
     assert cx.lib.nbx_spots_batch(cx.handle, arr, 3, 0, N.OUT_F32, ptrs, 0, C.byref(bad)) == 0
     for c, o in zip(ctxs, outs):
         assert np.array_equal(o, run(c).data)
+
+
+def test_concurrent_host_threads_share_one_context(gpu):
+    """Python threads calling the drop-in API at once (ctypes drops the GIL) serialise on the
+    context lock: every thread's images equal the same images rendered one after another."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2205_07976_b200 import image_stats, simulate_image
+
+    panel = synthetic.roi(synthetic.rayonix_panel(), 700, 900, 48, 64)
+    ctxs = [synthetic.ls49_context(synthetic.SEED + i, panel=panel, n_channels=6, n_domains=2,
+                                   compute=("fp32", "fp64")[i % 2]) for i in range(8)]
+
+    def render(c):
+        a = run(c, "f32").data.copy()
+        b = simulate_image(c).data.copy()
+        return a, b, image_stats(PixelBuffer(c.panel.dims, "f64", b)).total
+
+    serial = [render(c) for c in ctxs]
+    with ThreadPoolExecutor(8) as pool:
+        threaded = list(pool.map(render, ctxs * 3))
+    for i, (a, b, t) in enumerate(threaded):
+        sa, sb, st = serial[i % len(ctxs)]
+        assert np.array_equal(a, sa) and np.array_equal(b, sb) and t == st
