@@ -37,7 +37,7 @@ STEP_INSTR = 126  # FP-pipe instructions per step, SURVEY §8 D1 (FMA = 1)
 # What the implementation actually issues per step on its bounding pipe, counted in the
 # SASS of the hot loop (tools/sass_loop.py), by nbx_plan_info_t.kernel_variant:
 #   (pipe, pipe lane-ops per step, lanes per SM per clock of that pipe)
-IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 28, 64)}
+IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 22, 64)}
 SMS = 148
 
 

@@ -411,35 +411,68 @@ __device__ __forceinline__ AxisRec axis_rec(double S, double iv0, double delta, 
 
 __device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu; }
 
+// The Fhkl index of the recurrence loop comes from FP32 brackets instead of the
+// exact FP64 h: per (sub-pixel, domain) S+ = fl32(S (1 + 2^-20)), S- = fl32(S (1 - 2^-20)),
+// and per channel ONE packed FFMA2 rounds (S+ iv, S- iv) onto the integer grid
+// (+ 1.5 * 2^23).  fl32 of S, of iv and of the product perturb h by < 3 * 2^-24 |h|,
+// so S- iv and S+ iv bracket the exact h; when both round to the same integer n no
+// half-integer lies between them and round_half_away(h) = n (kernels.py:145-146).
+// Otherwise (|h| within ~2e-6 |h| of a half-integer: ~1e-4 of the channels) the
+// channel takes the exact path below.  Saves 6 FP64-pipe ops, 3 conversions and 6
+// issue slots per channel against the FP64 index.
+constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
+constexpr double kBracket = 0x1p-20;
+
 // One channel from the three axes' current sines: w F^2 F_latt^2.
 template <int IDX>
-__device__ __forceinline__ double rec_channel(const SpotsParams& P, const double* __restrict__ tab, int l0,
-                                              double2 c, double Sa, double Sb, double Sc, double ad, double an,
-                                              double bd, double bn, double cd, double cn) {
-    const double ha = Sa * c.x, hb = Sb * c.x, hc = Sc * c.x;  // kernels.py:257-260
-    const int ia = __double2int_rz(ha + copysign(0.5, ha));      // round half away (kernels.py:145-146)
-    const int ib = __double2int_rz(hb + copysign(0.5, hb));
-    const int ic = __double2int_rz(hc + copysign(0.5, hc));
+__device__ __forceinline__ double rec_channel(const SpotsParams& P, const double* __restrict__ tab, uint32_t kbias,
+                                              double2 c, float ivf, f2x SA, f2x SB, f2x SC, double Sa, double Sb,
+                                              double Sc, double ad, double an, double bd, double bn, double cd,
+                                              double cn) {
+    const f2x m = bc2(kMagicF32), iv2 = bc2(ivf);
+    const f2x ra = fma2(SA, iv2, m), rb = fma2(SB, iv2, m), rc = fma2(SC, iv2, m);
+    uint32_t ba = (uint32_t)ra, bb = (uint32_t)rb, bcx = (uint32_t)rc;
+    const bool ambiguous = (ba != (uint32_t)(ra >> 32)) | (bb != (uint32_t)(rb >> 32)) |
+                           (bcx != (uint32_t)(rc >> 32));
     double nn = (an * bn) * cn;
     double dd = (ad * bd) * cd;
-    if (min(min(abs_hi(ad), abs_hi(bd)), abs_hi(cd)) < kRecSmallHi) {
-        // near a Bragg plane: the exact reduced-phase form (both carry 1/pi^3: same ratio)
-        const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
-        const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
-        const AxisF64 e = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
-        nn = (a.num * b.num) * e.num;
-        dd = (a.den * b.den) * e.den;
+    const bool small = min(min(abs_hi(ad), abs_hi(bd)), abs_hi(cd)) < kRecSmallHi;
+    if (ambiguous | small) {  // rare: exact index and / or exact reduced phase
+        asm volatile("");     // keep the exact work inside the branch (no if-conversion)
+        const double ha = Sa * c.x, hb = Sb * c.x, hc = Sc * c.x;  // kernels.py:257-260
+        ba = kMagicBits + (uint32_t)__double2int_rz(ha + copysign(0.5, ha));  // kernels.py:145-146
+        bb = kMagicBits + (uint32_t)__double2int_rz(hb + copysign(0.5, hb));
+        bcx = kMagicBits + (uint32_t)__double2int_rz(hc + copysign(0.5, hc));
+        if (small) {
+            // near a Bragg plane: the exact reduced-phase form (both carry 1/pi^3: same ratio)
+            const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
+            const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
+            const AxisF64 e = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
+            nn = (a.num * b.num) * e.num;
+            dd = (a.den * b.den) * e.den;
+        }
     }
     const double ratio = nn * rcp_f64<kNewtonF64>(dd);
-    return (f2_f64<IDX>(P, tab, l0, ia, ib, ic) * c.y) * (ratio * ratio);
+    double F2;
+    if constexpr (IDX == kIdxHash)
+        F2 = f2_f64<IDX>(P, tab, 0, (int)(ba - kMagicBits), (int)(bb - kMagicBits), (int)(bcx - kMagicBits));
+    else  // (ba - M) sH + (bb - M) sK + (bc - M) - l0, mod 2^32 (the cell number is < 2^31)
+        F2 = __ldg(tab + (int)(ba * (uint32_t)P.sH + bb * (uint32_t)P.sK + bcx - kbias));
+    return (F2 * c.y) * (ratio * ratio);
+}
+
+__device__ __forceinline__ f2x bracket(double S) {
+    return pk2(__double2float_rn(S * (1.0 + kBracket)), __double2float_rn(S * (1.0 - kBracket)));
 }
 
 template <int IDX>
 __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const double2* __restrict__ sch,
-                                                     const RunF64* __restrict__ sru, double Sa, double Sb,
-                                                     double Sc) {
+                                                     const RunF64* __restrict__ sru, const float* __restrict__ sivf,
+                                                     double Sa, double Sb, double Sc) {
     const double* __restrict__ tab = static_cast<const double*>(P.table);
     const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
+    const uint32_t kbias = kMagicBits * (uint32_t)(P.sH + P.sK + 1) + (uint32_t)l0;
+    const f2x SA = bracket(Sa), SB = bracket(Sb), SC = bracket(Sc);
     double acc = 0.0;
     for (int ri = 0; ri < P.n_runs; ++ri) {
         const RunF64 run = sru[ri];
@@ -448,8 +481,8 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
         AxisRec C = axis_rec(Sc, run.iv0, run.delta, P.n_cells_d[2]);
 #pragma unroll kRecUnroll
         for (int w = run.begin; w < run.end; ++w) {
-            acc += rec_channel<IDX>(P, tab, l0, sch[w], Sa, Sb, Sc, A.den.s, A.num.s, B.den.s, B.num.s, C.den.s,
-                               C.num.s);
+            acc += rec_channel<IDX>(P, tab, kbias, sch[w], sivf[w], SA, SB, SC, Sa, Sb, Sc, A.den.s, A.num.s,
+                                    B.den.s, B.num.s, C.den.s, C.num.s);
             advance(A.den);
             advance(A.num);
             advance(B.den);
@@ -482,6 +515,8 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
         if constexpr (COMPUTE == 2) {
             RunF64* r = reinterpret_cast<RunF64*>(smem_raw + 16 * P.n_src);
             for (int i = tid; i < P.n_runs; i += kBlockX * kBlockY) r[i] = P.runs[i];
+            float* v = reinterpret_cast<float*>(smem_raw + 16 * P.n_src + sizeof(RunF64) * P.n_runs);
+            for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) v[i] = __double2float_rn(g[i].x);
         }
     }
     __syncthreads();
@@ -542,7 +577,9 @@ __global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCK
                     } else if constexpr (COMPUTE == 2) {
                         const double2* sch = reinterpret_cast<const double2*>(smem_raw);
                         double a = domain_sum_f64_rec<IDX>(
-                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), Sa, Sb, Sc);
+                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src),
+                            reinterpret_cast<const float*>(smem_raw + 16 * P.n_src + sizeof(RunF64) * P.n_runs),
+                            Sa, Sb, Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;
                     } else {
@@ -721,7 +758,7 @@ cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, 
                                : launch_shape<0, kIdxWide>(P, shape, smem, st);
     }
     if (compute == 4) {  // FP64 channel recurrence (sincg)
-        const size_t smem = (size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64);
+        const size_t smem = (size_t)P.n_src * 20 + (size_t)P.n_runs * sizeof(RunF64);  // + FP32 1/lambda
         return idx == kIdxHash ? launch_t<2, 0, kIdxHash, kPolyF32>(P, smem, st)
                                : launch_t<2, 0, kIdxWide, kPolyF32>(P, smem, st);
     }
