@@ -20,6 +20,7 @@
 //   IDX: Fhkl index kind -- magic-float bit patterns on a power-of-two grid, integer
 //     index on a dense grid, or the sparse hash table.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 #include <cstdint>
 
 #include "nbx_device.cuh"
@@ -40,18 +41,58 @@ enum { kOutF32 = 0, kOutF64 = 1, kOutAddF64 = 2, kOutRawF64 = 3, kOutImageF64 = 
 // np.interp (NumPy arr_interp) with len(xp) <= len(x) precomputes
 // slope_j = (fp[j+1]-fp[j]) / (xp[j+1]-xp[j]) and returns slope_j*(x-xp[j]) + fp[j]
 // for xp[j] <= x < xp[j+1]; the host precomputes the same slopes (P.bg_fs =
-// {fp_j, slope_j}), so the device value is the same arithmetic.  The interval
-// is found by walking from the previous source's (stol moves little between
-// sources; spectra are usually sorted), not by a fresh binary search.
+// {fp_j, slope_j}), so the device value is the same arithmetic.
+//
+// Per source the loop does no memory access beyond the (broadcast) source record:
+// the current interval [lo, hi) with its anchor, value and slope lives in registers
+// and is re-fetched only when stol leaves it (rarely: stol moves little between
+// sources).  The clamped ends are intervals too -- (-inf, xp_0) and [xp_{n-1}, inf)
+// with slope 0: fp + 0 * (x - anchor) is fp exactly, as np.interp returns.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double interp_profile(const double* __restrict__ xp, const double2* __restrict__ fs, int n,
-                                                 double x, int& j) {
-    if (x <= __ldg(xp)) return __ldg(fs).x;
-    if (x >= __ldg(xp + n - 1)) return __ldg(fs + n - 1).x;
-    while (__ldg(xp + j + 1) <= x) ++j;  // xp[j] <= x < xp[j+1], 0 <= j <= n-2
-    while (__ldg(xp + j) > x) --j;
-    const double2 f = __ldg(fs + j);
-    return __dadd_rn(__dmul_rn(f.y, x - __ldg(xp + j)), f.x);  // NumPy: no FMA contraction
+struct InterpCursor {
+    double lo, hi, anchor, f, slope;
+    int j;  // interval: -1 below xp_0, n-1 at/above xp_{n-1}
+};
+
+__device__ __forceinline__ void interp_seek(const double* __restrict__ xp, const double2* __restrict__ fs, int n,
+                                            double x, InterpCursor& c) {
+    int j = c.j;
+    if (x < __ldg(xp)) {
+        j = -1;
+    } else if (x >= __ldg(xp + n - 1)) {
+        j = n - 1;
+    } else {  // xp[j] <= x < xp[j+1], 0 <= j <= n-2, walked from the previous interval
+        j = min(max(j, 0), n - 2);
+        while (__ldg(xp + j + 1) <= x) ++j;
+        while (__ldg(xp + j) > x) --j;
+    }
+    c.j = j;
+    if (j < 0) {
+        c.lo = -CUDART_INF;
+        c.hi = c.anchor = __ldg(xp);
+        c.f = __ldg(fs).x;
+        c.slope = 0.0;
+    } else if (j >= n - 1) {
+        c.lo = c.anchor = __ldg(xp + n - 1);
+        c.hi = CUDART_INF;
+        c.f = __ldg(fs + n - 1).x;
+        c.slope = 0.0;
+    } else {
+        const double2 f = __ldg(fs + j);
+        c.lo = c.anchor = __ldg(xp + j);
+        c.hi = __ldg(xp + j + 1);
+        c.f = f.x;
+        c.slope = f.y;
+    }
+}
+
+// x / d correctly rounded from inv = RN(1/d): q0 = RN(x inv) is within an ulp,
+// r = x - q0 d is exact (FMA), and RN(q0 + r inv) is the IEEE quotient (Markstein;
+// x, d positive normal here).  Three FP64 ops instead of an iterative division.
+__device__ __forceinline__ double div_exact(double x, double d, double inv) {
+    const double q0 = __dmul_rn(x, inv);
+    const double r = __fma_rn(-q0, d, x);
+    return __fma_rn(r, inv, q0);
 }
 
 __device__ __forceinline__ double background_value(const SpotsParams& P, const DevPanel& pan, int sl, int f) {
@@ -70,11 +111,20 @@ __device__ __forceinline__ double background_value(const SpotsParams& P, const D
     if (P.pol_on) op *= 0.5 * (1.0 + c2t * c2t);
     const double sin_theta = sqrt(0.5 * (1.0 - c2t));
     double acc = 0.0;
-    int j = 0;
+    InterpCursor cur;
+    cur.j = 0;
+    cur.lo = CUDART_INF;  // empty: the first source seeks
+    cur.hi = -CUDART_INF;
     for (int w = 0; w < P.n_bg_chan; ++w) {
-        const double2 lw = __ldg(P.bg_chan + w);  // {lambda, weight}
-        const double fbg = interp_profile(P.bg_stol, P.bg_fs, P.bg_points, sin_theta / lw.x, j);
-        acc = __dadd_rn(acc, __dmul_rn(lw.y, fbg * fbg));  // acc += weights[w] * (f_bg * f_bg)
+        const double2 li = __ldg(reinterpret_cast<const double2*>(P.bg_chan + w));  // {lambda, 1/lambda}
+        const double wt = __ldg(&P.bg_chan[w].weight);
+        const double x = div_exact(sin_theta, li.x, li.y);  // sin_theta / lambda
+        if (!(x >= cur.lo && x < cur.hi)) {  // also NaN (np.interp propagates it; so does acc)
+            interp_seek(P.bg_stol, P.bg_fs, P.bg_points, x, cur);
+            if (isnan(x)) cur.f = x;
+        }
+        const double fbg = __dadd_rn(__dmul_rn(cur.slope, x - cur.anchor), cur.f);  // NumPy: no FMA contraction
+        acc = __dadd_rn(acc, __dmul_rn(wt, fbg * fbg));  // acc += weights[w] * (f_bg * f_bg)
     }
     return P.bg_scale * acc * op;
 }

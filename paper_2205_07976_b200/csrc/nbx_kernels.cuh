@@ -34,6 +34,12 @@ struct ChunkF32 {
 
 // FP64 path, channel-recurrence variant: sorted channels [begin, end) whose
 // 1/lambda are an arithmetic progression iv0 + k*delta (to 1e-14 in phase).
+// One source of the background stage: lambda, its correctly rounded reciprocal (for the
+// exact division, nbx_kernels.cu:div_exact) and the weight.
+struct BgChan {
+    double lambda, inv_lambda, weight, pad;
+};
+
 struct RunF64 {
     double iv0, delta;
     int32_t begin, end;
@@ -73,7 +79,7 @@ struct SpotsParams {
     int32_t max_slow, max_fast;    // launch covers rows [row0, max_slow) of every panel
     int32_t row0, pad2;            // first row of this launch (row bands of a pipelined run)
     // diffuse background (kernels.py:279-312)
-    const double2* bg_chan;        // {lambda, w} of every source
+    const BgChan* bg_chan;         // {lambda, 1/lambda, w} of every source
     const double* bg_stol;
     const double2* bg_fs;          // {f_bg, slope to the next point} per profile point
     int32_t n_bg_chan;

@@ -350,14 +350,13 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
     }
     if (!finite(d->bg_thickness_factor)) throw ArgError("thickness_factor must be finite");
     double wsum = 0.0;
-    std::vector<double> lw(2 * (size_t)d->n_sources);
+    std::vector<nbx::BgChan> lw(d->n_sources);
     for (int i = 0; i < d->n_sources; ++i) {
-        lw[2 * i] = d->wavelengths[i];
-        lw[2 * i + 1] = d->weights[i];
+        lw[i] = nbx::BgChan{d->wavelengths[i], 1.0 / d->wavelengths[i], d->weights[i], 0.0};
         wsum += d->weights[i];
     }
-    B.chan.ensure(lw.size() * sizeof(double));
-    NBX_CUDA(cudaMemcpy(B.chan.p, lw.data(), lw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    B.chan.ensure(lw.size() * sizeof(nbx::BgChan));
+    NBX_CUDA(cudaMemcpy(B.chan.p, lw.data(), lw.size() * sizeof(nbx::BgChan), cudaMemcpyHostToDevice));
     // {f_j, slope_j}: np.interp's own precomputed slopes (same IEEE expression)
     std::vector<double> fs(2 * (size_t)d->bg_points, 0.0);
     for (int i = 0; i < d->bg_points; ++i) {
@@ -369,7 +368,7 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
     B.f.ensure(sizeof(double) * fs.size());
     NBX_CUDA(cudaMemcpy(B.stol.p, d->bg_stol, sizeof(double) * d->bg_points, cudaMemcpyHostToDevice));
     NBX_CUDA(cudaMemcpy(B.f.p, fs.data(), sizeof(double) * fs.size(), cudaMemcpyHostToDevice));
-    P.bg_chan = static_cast<const double2*>(B.chan.p);
+    P.bg_chan = static_cast<const nbx::BgChan*>(B.chan.p);
     P.bg_stol = static_cast<const double*>(B.stol.p);
     P.bg_fs = static_cast<const double2*>(B.f.p);
     P.n_bg_chan = d->n_sources;

@@ -147,3 +147,22 @@ def test_stats_restatement_is_the_reference():
         assert total == ref[3]
         assert total / n == ref[2]
         assert float(v.min()) == ref[0] and float(v.max()) == ref[1]
+
+
+def test_background_division_identity_is_correctly_rounded():
+    """The background kernel's sin(theta)/lambda (nbx_kernels.cu:div_exact): q0 = RN(x inv),
+    r = x - q0 lambda (exact, FMA), RN(q0 + r inv) with inv = RN(1/lambda) equals the IEEE
+    quotient NumPy computes.  Checked with exact rational arithmetic on seeded samples over the
+    range the kernel sees (x = sin(theta) in [0, 1], lambda in Angstrom)."""
+    import random
+    from fractions import Fraction
+
+    rng = random.Random(7)
+    for i in range(20000):
+        x = rng.random() if i % 2 else math.sqrt(0.5 * (1 - rng.uniform(-1, 1)))
+        lam = rng.uniform(0.2, 5.0) if i % 3 else 12398.419843 / rng.uniform(4000, 15000)
+        inv = 1.0 / lam
+        q0 = x * inv
+        r = float(Fraction(x) - Fraction(q0) * Fraction(lam))
+        q = float(Fraction(r) * Fraction(inv) + Fraction(q0))
+        assert q == x / lam, (x, lam)
