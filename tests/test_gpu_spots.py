@@ -597,3 +597,35 @@ def test_concurrent_host_threads_share_one_context(gpu):
     for i, (a, b, t) in enumerate(threaded):
         sa, sb, st = serial[i % len(ctxs)]
         assert np.array_equal(a, sa) and np.array_equal(b, sb) and t == st
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_ragged_multi_panel_and_single_pixel_panels(gpu, compute):
+    """Edge shapes: panels of 1, 7 and 1031 rows (ragged: not a multiple of the 8-row block
+    line, one panel a single pixel row) sharing 19 columns, and a 1x1 panel -- against the
+    oracle and, panel by panel, against single-panel runs (bit for bit)."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import Detector
+
+    base = synthetic.roi(synthetic.rayonix_panel(), 700, 900, 8, 19)
+    panels = tuple(dataclasses.replace(base, slow_pixels=n, beam_center=(base.beam_center[0] - 40 * k,
+                                                                         base.beam_center[1] + 3 * k))
+                   for k, n in enumerate((1, 7, 1031)))
+    det = Detector(panels)
+    ctx = synthetic.ls49_context(panel=det, n_channels=5, n_domains=2, compute=compute)
+    tol = FP64_TOL if compute == "fp64" else FP32_TOL
+    want, _ = oracle.spots(describe(dataclasses.replace(ctx, panel=Detector(panels[:2]))), "f64")
+    got = run(ctx, "f64").data
+    m = parity.metrics(got[: 8 * 19], want, (8, 19))
+    assert m["total"] < tol, m
+    off = 0
+    for p in panels:
+        single = run(dataclasses.replace(ctx, panel=p), "f64").data
+        assert np.array_equal(single, got[off: off + single.size])
+        off += single.size
+    one = dataclasses.replace(base, slow_pixels=1, fast_pixels=1)
+    c1 = dataclasses.replace(ctx, panel=one)
+    w1, _ = oracle.spots(describe(c1), "f64")
+    g1 = run(c1, "f64").data
+    assert abs(g1[0] - w1[0]) <= tol * abs(w1[0]) + 1e-300
