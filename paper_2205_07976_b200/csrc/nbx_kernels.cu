@@ -487,20 +487,19 @@ __device__ __forceinline__ double rec_channel(const SpotsParams& P, const double
     double nn = (an * bn) * cn;
     double dd = (ad * bd) * cd;
     const bool small = min(min(abs_hi(ad), abs_hi(bd)), abs_hi(cd)) < kRecSmallHi;
-    if (ambiguous | small) {  // rare: exact index and / or exact reduced phase
+    if (ambiguous | small) {  // rare: the exact index and the exact reduced-phase form
         asm volatile("");     // keep the exact work inside the branch (no if-conversion)
         const double ha = Sa * c.x, hb = Sb * c.x, hc = Sc * c.x;  // kernels.py:257-260
         ba = kMagicBits + (uint32_t)__double2int_rz(ha + copysign(0.5, ha));  // kernels.py:145-146
         bb = kMagicBits + (uint32_t)__double2int_rz(hb + copysign(0.5, hb));
         bcx = kMagicBits + (uint32_t)__double2int_rz(hc + copysign(0.5, hc));
-        if (small) {
-            // near a Bragg plane: the exact reduced-phase form (both carry 1/pi^3: same ratio)
-            const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
-            const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
-            const AxisF64 e = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
-            nn = (a.num * b.num) * e.num;
-            dd = (a.den * b.den) * e.den;
-        }
+        // near a Bragg plane (or an ambiguous index: cheaper than a second predicate per
+        // channel): the exact reduced-phase form (both carry 1/pi^3: same ratio)
+        const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
+        const AxisF64 b = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
+        const AxisF64 e = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
+        nn = (a.num * b.num) * e.num;
+        dd = (a.den * b.den) * e.den;
     }
     const double ratio = nn * rcp_f64<kNewtonF64>(dd);
     double F2;
