@@ -315,6 +315,9 @@ def run_ours(args):
         "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
                      "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
                      "traffic": traffic,
+                     "traffic_note": "ncu dram read+write bytes of one spot launch (profiles/ncu_summary.json): "
+                                     "reads are the L2-resident inputs once; most of the image write-back is "
+                                     "still in the 126 MB L2 when the kernel ends, so traffic < writeback bytes",
                      # the image write-back (the path's only HBM stream; north_star asks for it)
                      "writeback": {"bytes_per_image": int(plans[0].n_pixels) * 4,
                                    "gbs": plans[0].n_pixels * 4 / (mean_kernel / 1e3) / 1e9},
