@@ -3,7 +3,9 @@
 usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py
 Covers: FP32 MUFU / polynomial / degree-4 numerators, FP64 direct and recurrence, the
 non-grating shapes, the wide (integer) index, thickness layers + multi-panel, background
-fused into the image, the banded (pipelined) host download, add_array, noise, stats.
+fused into the image, the banded (pipelined) host download, add_array, noise, stats, the
+standalone background, the sparse Fhkl table, several FP64 recurrence runs, channel-shard
+partials with finalize and the slot reduction, and the pipelined campaign.
 """
 import dataclasses
 import os
@@ -58,4 +60,39 @@ add_array(acc, spots)
 add_noise(spots, seed=5)
 image_stats(img)
 image_histogram(img, 16, (0.0, float(img.data.max()) + 1.0))
+# standalone background, sparse Fhkl table, FP64 recurrence with several runs
+from paper_2205_07976_b200 import add_background  # noqa: E402
+
+bg = PixelBuffer.zeros(roi.dims, "f32")
+add_background(WATER, ctx.panel, ctx.spectrum, 1.0, bg)
+os.environ["NBX_FHKL_HASH"] = "1"
+for compute in ("fp32", "fp64"):
+    run(synthetic.ls49_context(panel=roi, n_channels=16, n_domains=2, compute=compute))
+del os.environ["NBX_FHKL_HASH"]
+two_runs = synthetic.ls49_context(panel=roi, n_channels=200, n_domains=1, compute="fp64")
+run(two_runs)
+# channel shards: RAW partials + finalize, and the peer-memory slot reduction (one process)
+import torch  # noqa: E402
+
+whole = SpotsPlan(ctx)
+raw = torch.zeros(2 * whole.n_pixels, dtype=torch.float64, device="cuda")
+n_src = len(ctx.spectrum.samples)
+for r, (lo, hi) in enumerate(((0, n_src // 2), (n_src // 2, n_src))):
+    part = SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=0.0)
+    part.run(raw.data_ptr() + r * whole.n_pixels * 8, mode=N.OUT_RAW_STORE_F64, on_device=True)
+cx = N.context()
+out = np.zeros(whole.n_pixels, np.float32)
+bad = N.C.c_int64(-1)
+assert cx.lib.nbx_reduce_slots(cx.handle, raw.data_ptr(), 2, whole.n_pixels, whole.scale, N.OUT_F32,
+                               out.ctypes.data, 0, N.C.byref(bad)) == 0
+assert cx.lib.nbx_finalize(cx.handle, raw.data_ptr(), whole.n_pixels, whole.scale, N.OUT_F32, out.ctypes.data, 0,
+                           N.C.byref(bad)) == 0
+# the pipelined campaign (double-buffered download, CRC-32, file writes)
+import tempfile  # noqa: E402
+
+from paper_2205_07976_b200.io import run_campaign  # noqa: E402
+
+with tempfile.TemporaryDirectory() as d:
+    run_campaign(lambda i: synthetic.ls49_context(synthetic.SEED + i, panel=roi, n_channels=4, n_domains=2), 3, d,
+                 background=WATER)
 print("sanitize run complete", flush=True)
