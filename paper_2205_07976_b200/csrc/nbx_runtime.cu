@@ -187,7 +187,10 @@ struct Plan {
 bool finite(double x) { return std::isfinite(x); }
 
 bool trace_enabled() {
-    static const bool on = std::getenv("NBX_TRACE") != nullptr;
+    static const bool on = [] {
+        const char* v = std::getenv("NBX_TRACE");
+        return v != nullptr && *v != '\0' && std::strcmp(v, "0") != 0;
+    }();
     return on;
 }
 
