@@ -8,4 +8,4 @@ for a in "$@"; do
   echo "== $a" >> gpurun_out/extra.log
   timeout 600 bash -c "$a" >> gpurun_out/extra.log 2>&1; echo "rc=$?" >> gpurun_out/extra.log
 done
-tail -3 gpurun_out/smoke.log; tail -30 gpurun_out/pytest_gpu.log; tail -40 gpurun_out/extra.log 2>/dev/null
+tail -3 gpurun_out/smoke.log; tail -30 gpurun_out/pytest_gpu.log; tail -40 gpurun_out/extra.log 2>/dev/null || true
