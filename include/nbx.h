@@ -225,7 +225,8 @@ int nbx_background(void* ctx, const nbx_spots_desc* d, int out_mode, void* out, 
                    int64_t* first_bad);
 
 /* Scale + store a reduced raw FP64 image (root of a channel-sharded image,
- * SURVEY §8 E1): out = mode(scale * raw).  raw is a device pointer. */
+ * SURVEY §8 E1): out = mode(scale * raw), mode F32, F64 or ADD_F64.  raw is a device
+ * pointer. */
 int nbx_finalize(void* ctx, const double* raw, int64_t n, double scale, int out_mode,
                  void* out, int out_on_device, int64_t* first_bad);
 

@@ -1506,8 +1506,8 @@ int nbx_finalize(void* ctxp, const double* raw, int64_t n, double scale, int out
     int st = guarded(ctxp, [&] {
         if (!ctxp) throw ArgError("NULL context");
         if (!raw || !out || n < 0) throw ArgError("invalid finalize arguments");
-        if (out_mode == NBX_OUT_RAW_F64) throw ArgError("finalize cannot write a raw image");
-        check_mode(out_mode);
+        if (out_mode != NBX_OUT_F32 && out_mode != NBX_OUT_F64 && out_mode != NBX_OUT_ADD_F64)
+            throw ArgError("finalize output mode must be F32, F64 or ADD_F64");
         Ctx* ctx = static_cast<Ctx*>(ctxp);
         NBX_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;

@@ -629,3 +629,44 @@ def test_ragged_multi_panel_and_single_pixel_panels(gpu, compute):
     w1, _ = oracle.spots(describe(c1), "f64")
     g1 = run(c1, "f64").data
     assert abs(g1[0] - w1[0]) <= tol * abs(w1[0]) + 1e-300
+
+
+def test_c_abi_argument_errors_leave_the_context_usable(gpu):
+    """Every entry point rejects bad arguments with NBX_ERR_ARG and a message (no crash, no
+    out-of-bounds write), and the context keeps working afterwards (include/nbx.h contract)."""
+    from paper_2205_07976_b200 import _native as N
+
+    cx = N.context()
+    lib, h = cx.lib, cx.handle
+    ctx = synthetic.c1_context()
+    desc = describe(ctx)
+    out = np.zeros(ctx.panel.n_pixels, np.float32)
+    bad = N.C.c_int64(-1)
+    dev = N.C.c_void_p()
+    calls = {
+        "spots NULL ctx": lambda: lib.nbx_spots(None, N.C.byref(desc.c), 0, 0, out.ctypes.data, 0, N.C.byref(bad)),
+        "spots NULL desc": lambda: lib.nbx_spots(h, None, 0, 0, out.ctypes.data, 0, N.C.byref(bad)),
+        "spots NULL out": lambda: lib.nbx_spots(h, N.C.byref(desc.c), 0, 0, None, 0, N.C.byref(bad)),
+        "spots mode": lambda: lib.nbx_spots(h, N.C.byref(desc.c), 0, 9, out.ctypes.data, 0, N.C.byref(bad)),
+        "spots compute": lambda: lib.nbx_spots(h, N.C.byref(desc.c), 7, 0, out.ctypes.data, 0, N.C.byref(bad)),
+        "plan_run NULL": lambda: lib.nbx_plan_run(None, 0, out.ctypes.data, 0, N.C.byref(bad)),
+        "finalize image mode": lambda: lib.nbx_finalize(h, out.ctypes.data, out.size, 1.0, N.OUT_IMAGE_F32,
+                                                        out.ctypes.data, 0, N.C.byref(bad)),
+        "reduce_slots raw mode": lambda: lib.nbx_reduce_slots(h, out.ctypes.data, 1, out.size, 1.0, N.OUT_RAW_F64,
+                                                              out.ctypes.data, 0, N.C.byref(bad)),
+        "stats empty": lambda: lib.nbx_image_stats(h, out.ctypes.data, 0, 0, 0, (N.C.c_double * 4)()),
+        "noise dtype": lambda: lib.nbx_add_noise(h, out.ctypes.data, out.ctypes.data, out.size, 7, 1, 0, 0),
+        "background mode": lambda: lib.nbx_background(h, N.C.byref(desc.c), N.OUT_IMAGE_F64, out.ctypes.data, 0,
+                                                      N.C.byref(bad)),
+        "campaign count": lambda: lib.nbx_campaign(h, N.C.byref(desc.c), -1, 0, None, None, N.C.byref(bad)),
+        "ipc_open NULL": lambda: lib.nbx_ipc_open(h, None, N.C.byref(dev)),
+        "ipc_alloc size": lambda: lib.nbx_ipc_alloc(h, 0, N.C.byref(dev), N.C.create_string_buffer(64)),
+    }
+    for name, call in calls.items():
+        assert call() == N.NBX_ERR_ARG, name
+        if "NULL ctx" not in name and "plan_run" not in name:
+            assert cx.error(), name
+    ref = run(ctx).data
+    again = PixelBuffer.zeros(ctx.panel.dims)
+    nanobragg_spots(ctx, again)
+    assert np.array_equal(again.data, ref)
