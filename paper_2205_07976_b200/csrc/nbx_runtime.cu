@@ -1619,7 +1619,8 @@ int nbx_add_array(void* ctxp, double* lhs, const float* rhs, int64_t n, int on_d
             NBX_CUDA(cudaStreamSynchronize(s));
             return NBX_OK;
         }
-        DevBuf dl, dr;
+        DevBuf& dl = ctx->out_scratch;  // persistent scratch: a per-call cudaMalloc/cudaFree pair
+        DevBuf& dr = ctx->stage_in;     // costs more than the whole kernel
         dl.ensure((size_t)n * 8);
         dr.ensure((size_t)n * 4);
         NBX_CUDA(cudaMemcpyAsync(dl.p, lhs, (size_t)n * 8, cudaMemcpyHostToDevice, s));
@@ -1647,7 +1648,8 @@ int nbx_add_noise(void* ctxp, const void* mean, void* out, int64_t n, int dtype,
             NBX_CUDA(cudaStreamSynchronize(s));
             return NBX_OK;
         }
-        DevBuf dm, dout;
+        DevBuf& dm = ctx->stage_in;  // persistent scratch (see nbx_add_array)
+        DevBuf& dout = ctx->out_scratch;
         dm.ensure(bytes);
         dout.ensure(bytes);
         NBX_CUDA(cudaMemcpyAsync(dm.p, mean, bytes, cudaMemcpyHostToDevice, s));
