@@ -107,3 +107,29 @@ def test_large_8k_image_bands_and_offsets(gpu, compute):
         out = PixelBuffer.zeros(sub.dims, "f32")
         nanobragg_spots(dataclasses.replace(ctx, panel=sub), out)
         assert np.array_equal(out.data.reshape(sub.dims), img[r0:r0 + 7])
+
+
+def test_full_c4_fp32_vs_fp64_and_stripe_vs_oracle(gpu):
+    """The full C4 workload (256 Jungfrau-like thick panels, oversample 2, 3 parallax layers,
+    100 channels x 50 domains): the FP32 image against the FP64 image at the FP32 tolerance,
+    and one panel row of the FP64 image against the oracle at 1e-9 (size-independent
+    properties at the BASELINE size; the oracle runs only on the stripe)."""
+    det = synthetic.jungfrau_detector()
+    imgs = {}
+    for compute in ("fp64", "fp32"):
+        plan = SpotsPlan(synthetic.ls49_context(panel=det, compute=compute, oversample=2))
+        img = np.zeros(plan.n_pixels)
+        plan.run(img, mode=N.OUT_F64)
+        imgs[compute] = img
+        plan.close()
+    m = parity.metrics(imgs["fp32"], imgs["fp64"], det.dims)
+    assert m["n_spots"] > 20
+    assert m["total"] < 1e-4 and m["spot"] < 1e-4, m
+    # panel 120 (near the beam), rows 100..101: a stripe sub-panel through the oracle
+    p = det.panels[120]
+    stripe = dataclasses.replace(p, slow_pixels=2, beam_center=(p.beam_center[0] - 100, p.beam_center[1]))
+    ctx = synthetic.ls49_context(panel=stripe, compute="fp64", oversample=2)
+    want, _ = oracle.spots(describe(ctx), "f64")
+    off = 120 * p.slow_pixels * p.fast_pixels + 100 * p.fast_pixels
+    got = imgs["fp64"][off:off + want.size]
+    assert np.max(np.abs(got - want)) <= 1e-9 * np.max(np.abs(want)), (np.abs(got - want).max(), want.max())
