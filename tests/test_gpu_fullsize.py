@@ -133,3 +133,31 @@ def test_full_c4_fp32_vs_fp64_and_stripe_vs_oracle(gpu):
     off = 120 * p.slow_pixels * p.fast_pixels + 100 * p.fast_pixels
     got = imgs["fp64"][off:off + want.size]
     assert np.max(np.abs(got - want)) <= 1e-9 * np.max(np.abs(want)), (np.abs(got - want).max(), want.max())
+
+
+def test_full_c5_fp32_vs_fp64_and_channel_shards(gpu):
+    """The full C5 workload (one 3840^2 image, 1000 channels E_j = 7020 + 0.2 j eV, 50 domains):
+    FP32 vs FP64 at the FP32 tolerance, and the 4-way channel-sharded decomposition (each
+    shard an unscaled FP64 partial with the global normalisation, summed and scaled once --
+    what 4 GPUs compute) against the whole FP64 image at 1e-11."""
+    imgs = {}
+    for compute in ("fp64", "fp32"):
+        ctx = synthetic.ls49_context(n_channels=1000, de=0.2, e0=7020.0, compute=compute)
+        plan = SpotsPlan(ctx)
+        img = np.zeros(plan.n_pixels)
+        plan.run(img, mode=N.OUT_F64)
+        imgs[compute] = img
+        scale = plan.scale
+        plan.close()
+    m = parity.metrics(imgs["fp32"], imgs["fp64"], (3840, 3840))
+    assert m["n_spots"] > 50 and m["total"] < 1e-4 and m["spot"] < 1e-4, m
+    from paper_2205_07976_b200.parallel import channel_shards, global_norm
+
+    ctx = synthetic.ls49_context(n_channels=1000, de=0.2, e0=7020.0, compute="fp64")
+    raw = np.zeros(3840 * 3840)
+    for lo, hi in channel_shards(1000, 4):
+        part = SpotsPlan(ctx, src_begin=lo, src_end=hi, norm=global_norm(ctx))
+        part.run(raw, mode=N.OUT_RAW_F64)
+        part.close()
+    m = parity.metrics(raw * scale, imgs["fp64"], (3840, 3840))
+    assert m["total"] < 1e-11 and m["spot"] < 1e-11, m
