@@ -150,3 +150,23 @@ def test_default_device_follows_nbx_device_then_local_rank(monkeypatch):
     torch = __import__("sys").modules.get("torch")
     if torch is None or not torch.cuda.is_initialized():
         assert _native.default_device() == (5 % n if n else 0)
+
+
+def test_missing_native_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the library absent the drop-in call raises NativeError (a fresh
+    interpreter with NBX_LIB pointing at a missing file)."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2205_07976_b200 import PixelBuffer, nanobragg_spots, synthetic\n"
+            "from paper_2205_07976_b200.errors import NativeError\n"
+            "ctx = synthetic.c1_context()\n"
+            "try:\n"
+            "    nanobragg_spots(ctx, PixelBuffer.zeros(ctx.panel.dims))\n"
+            "except NativeError as e:\n"
+            "    print('NativeError', e)\n" % str(Path(__file__).resolve().parents[1]))
+    env = dict(__import__("os").environ, NBX_LIB=str(tmp_path / "absent.so"))
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert res.returncode == 0, res.stderr
+    assert res.stdout.startswith("NativeError native library missing"), res.stdout
