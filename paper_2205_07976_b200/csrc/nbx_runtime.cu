@@ -124,6 +124,7 @@ struct Ctx {
     DevBuf out_scratch;     // device image when the caller passes host memory
     DevBuf stage_in, stats_parts, stats_res, hist_counts;  // image_stats / image_histogram scratch
     DevBuf raw_scratch;     // FP64 partial of a long spectrum split into channel shards
+    DevBuf img_scratch;     // simulate_image accumulator of a long spectrum (device, f64)
     DevBuf fault;           // one u64
     std::string err;
 };
@@ -1178,11 +1179,12 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
     int64_t bad = -1;
     if (ctxp && d && d->n_sources > 0) {
         const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
-        if (se - sb > kMaxShardSources && out_mode != NBX_OUT_IMAGE_F64 && out_mode != NBX_OUT_IMAGE_F32) {
+        if (se - sb > kMaxShardSources) {
             // Long spectrum (the reference has no limit): channel shards accumulated as FP64
             // partials with the GLOBAL normalisation, then one scale + store -- exactly a
             // channel-sharded image on one device.  A RAW request receives
-            // the shards' partials added into the caller's buffer.
+            // the shards' partials added into the caller's buffer; an IMAGE request gets the
+            // simulate_image accumulator composed stage by stage (below).
             int64_t npix = 0;
             double scale = 0.0;
             const int st = guarded(ctxp, [&] {
@@ -1223,8 +1225,43 @@ int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, vo
                 return NBX_OK;
             });
             if (st != NBX_OK || out_mode == NBX_OUT_RAW_F64 || out_mode == NBX_OUT_RAW_STORE_F64) return st;
-            return nbx_finalize(ctxp, static_cast<const double*>(static_cast<Ctx*>(ctxp)->raw_scratch.p), npix, scale,
-                                out_mode, out, out_on_device, first_bad);
+            Ctx* ctx = static_cast<Ctx*>(ctxp);
+            const double* raw = static_cast<const double*>(ctx->raw_scratch.p);
+            if (out_mode != NBX_OUT_IMAGE_F64 && out_mode != NBX_OUT_IMAGE_F32)
+                return nbx_finalize(ctxp, raw, npix, scale, out_mode, out, out_on_device, first_bad);
+            // simulate_image's accumulator, the fused epilogue's stages one after another with
+            // the same arithmetic and fault precedence: f64(f32(spots)) (+ f64(f32(background)))
+            // (scheduler.py:156-183), then the f32 payload for IMAGE_F32 (io.py:403-434)
+            const bool direct = out_mode == NBX_OUT_IMAGE_F64 && out_on_device;
+            void* img = out;
+            int st2 = guarded(ctxp, [&] {
+                if (!direct) {
+                    ctx->img_scratch.ensure((size_t)npix * sizeof(double));
+                    img = ctx->img_scratch.p;
+                }
+                NBX_CUDA(cudaMemsetAsync(img, 0, (size_t)npix * sizeof(double), ctx->stream));
+                return NBX_OK;
+            });
+            if (st2 != NBX_OK) return st2;
+            ctx->fault_stage = 0;
+            st2 = nbx_finalize(ctxp, raw, npix, scale, NBX_OUT_ADD_F64, img, 1, first_bad);
+            if (st2 != NBX_OK) return st2;
+            if (d->bg_points > 0) {
+                st2 = nbx_background(ctxp, d, NBX_OUT_ADD_F64, img, 1, first_bad);  // sets fault_stage 1
+                if (st2 != NBX_OK) return st2;
+            }
+            if (out_mode == NBX_OUT_IMAGE_F64) {
+                if (direct) return NBX_OK;
+                return guarded(ctxp, [&] {
+                    NBX_CUDA(cudaMemcpy(out, img, (size_t)npix * sizeof(double),
+                                        out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+                    return NBX_OK;
+                });
+            }
+            st2 = nbx_finalize(ctxp, static_cast<const double*>(img), npix, 1.0, NBX_OUT_F32, out, out_on_device,
+                               first_bad);
+            if (st2 == NBX_ERR_NUMERICAL) ctx->fault_stage = 2;
+            return st2;
         }
     }
     int st = guarded(ctxp, [&] {
@@ -1322,7 +1359,7 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                  uint32_t* crcs, int64_t* first_bad) {
     if (first_bad) *first_bad = -1;
     int64_t bad_code = -1;
-    int st = guarded(ctxp, [&] {
+    int st = guarded(ctxp, [&]() -> int {
         if (!ctxp) throw ArgError("NULL context");
         if (n_images < 0 || (n_images > 0 && (!descs || !paths || !crcs))) throw ArgError("invalid campaign arguments");
         Ctx* ctx = static_cast<Ctx*>(ctxp);
@@ -1379,6 +1416,32 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
             for (int q = 0; q < 2; ++q) NBX_CUDA(cudaMallocHost(&ctx->camp_host[q], max_bytes));
             ctx->camp_host_bytes = max_bytes;
         }
+        auto write_image = [&](int i, const void* data, size_t nbytes) {
+            crcs[i] = crc32_update(0, static_cast<const unsigned char*>(data), nbytes);
+            FILE* fh = std::fopen(paths[i], "wb");
+            if (!fh) throw ArgError(std::string("cannot open ") + paths[i]);
+            const size_t wrote = std::fwrite(data, 1, nbytes, fh);
+            const int closed = std::fclose(fh);
+            if (wrote != nbytes || closed != 0) throw ArgError(std::string("short write to ") + paths[i]);
+        };
+        bool any_long = false;  // a spectrum longer than one launch: nbx_spots' sharded image path
+        for (int i = 0; i < n_images; ++i) {
+            const int sb = descs[i].src_begin, se = descs[i].src_end <= 0 ? descs[i].n_sources : descs[i].src_end;
+            any_long |= se - sb > kMaxShardSources;
+        }
+        if (any_long) {  // image by image, not pipelined (rare: > 8192 sources per image)
+            for (int i = 0; i < n_images; ++i) {
+                int64_t bad = -1;
+                const int s2 = nbx_spots(ctx, descs + i, compute, NBX_OUT_IMAGE_F32, ctx->camp_host[0], 0, &bad);
+                if (s2 == NBX_ERR_NUMERICAL) {
+                    bad_code = ((int64_t)i << 40) | bad;
+                    return NBX_OK;
+                }
+                if (s2 != NBX_OK) return s2;
+                write_image(i, ctx->camp_host[0], (size_t)count_pixels(descs + i) * 4);
+            }
+            return NBX_OK;
+        }
         if (n_images > 0) launch(0);
         for (int i = 0; i < n_images; ++i) {
             const int b = i & 1;
@@ -1392,17 +1455,11 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                 return NBX_OK;
             }
             const auto t0 = std::chrono::steady_clock::now();
-            crcs[i] = crc32_update(0, static_cast<const unsigned char*>(ctx->camp_host[b]), bytes[b]);
-            const auto t1 = std::chrono::steady_clock::now();
-            FILE* fh = std::fopen(paths[i], "wb");
-            if (!fh) throw ArgError(std::string("cannot open ") + paths[i]);
-            const size_t wrote = std::fwrite(ctx->camp_host[b], 1, bytes[b], fh);
-            const int closed = std::fclose(fh);
-            if (wrote != bytes[b] || closed != 0) throw ArgError(std::string("short write to ") + paths[i]);
+            write_image(i, ctx->camp_host[b], bytes[b]);
             if (trace_enabled()) {
-                const auto t2 = std::chrono::steady_clock::now();
-                auto ms = [](auto a, auto c) { return std::chrono::duration<double, std::milli>(c - a).count(); };
-                std::fprintf(stderr, "[nbx] campaign image %d: crc %.2f ms, write %.2f ms\n", i, ms(t0, t1), ms(t1, t2));
+                const auto t1 = std::chrono::steady_clock::now();
+                std::fprintf(stderr, "[nbx] campaign image %d: crc + write %.2f ms\n", i,
+                             std::chrono::duration<double, std::milli>(t1 - t0).count());
             }
         }
         return NBX_OK;

@@ -456,6 +456,24 @@ def test_long_spectrum_is_channel_sharded_on_one_device(gpu, compute):
     got, _ = oracle_check(ctx, FP64_TOL if compute == "fp64" else FP32_TOL)
     f32 = run(ctx, "f32").data
     np.testing.assert_allclose(f32, got, rtol=2.0 ** -23, atol=0)
+    # simulate_image / run_campaign on the long spectrum: the accumulator composed stage by
+    # stage equals f64(f32(spots)) + f64(f32(background)) bit for bit, and the campaign's
+    # .bin payload is that accumulator rounded to f32
+    import tempfile
+
+    from paper_2205_07976_b200 import BackgroundProfile, add_background, simulate_image
+    from paper_2205_07976_b200.io import read_image, run_campaign
+
+    water = BackgroundProfile(points=((0.0, 2.57), (0.07, 2.8), (0.12, 5.0), (0.3, 6.5)))
+    img = simulate_image(ctx, background=water, thickness_factor=0.8)
+    bg = PixelBuffer.zeros(panel.dims, "f32")
+    add_background(water, panel, spec, 0.8, bg)
+    want = f32.astype(np.float64) + bg.data.astype(np.float64)
+    assert np.array_equal(img.data, want)
+    with tempfile.TemporaryDirectory() as d:
+        res = run_campaign(lambda i: ctx, 2, d, background=water, thickness_factor=0.8)
+        for path in res.paths:
+            assert np.array_equal(read_image(path)[0].reshape(-1), want.astype(np.float32))
 
 
 def test_pipelined_image_mode_with_background_is_bitwise_the_device_image(gpu):
