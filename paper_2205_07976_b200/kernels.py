@@ -327,7 +327,24 @@ def simulate_image(ctx, background=None, thickness_factor: float = 1.0, out: Pix
     + f64(f32(background)) (add_array, kernels.py:315-331), with the spot and
     background stages evaluated by the same kernel and no 32-bit staging
     buffers in HBM.  ``background=None`` skips the background stage.
+
+    Also accepts the reference's own signature ``simulate_image(config, image_seed,
+    executor=None)`` with a ``SimulationConfig``-like ``config`` (``crystal_for_seed``,
+    ``panel``, ``spectrum``, ``oversample``, ``background``, ``thickness_factor``;
+    io.py:122-157), FP64 path as in the reference.  The executor then receives one
+    ("simulate_image", ms) record for the fused launch.
     """
+    if hasattr(ctx, "crystal_for_seed"):  # scheduler.py:156-183 signature
+        config, image_seed = ctx, background
+        if image_seed is None or isinstance(image_seed, bool):
+            raise TypeError("simulate_image(config, image_seed, executor=None) needs an integer image_seed")
+        if executor is None and not isinstance(thickness_factor, (int, float)):
+            executor = thickness_factor  # positional executor, the reference's third argument
+        sctx = SpotsContext(config.crystal_for_seed(int(image_seed)), config.panel, config.spectrum,
+                            int(getattr(config, "oversample", 1)))
+        return simulate_image(sctx, background=getattr(config, "background", None),
+                              thickness_factor=float(getattr(config, "thickness_factor", 1.0)), out=out,
+                              executor=executor)
     dims = ctx.panel.dims
     if out is None:
         out = PixelBuffer.zeros(dims, "f64")

@@ -114,3 +114,48 @@ def test_background_random_profiles_vs_oracle(gpu, seed):
     add_background(prof, panel, beam, tf, got32)
     want32 = want.astype(np.float32)
     assert np.all(np.abs(got32.data.view(np.int32).astype(np.int64) - want32.view(np.int32)) <= 1)
+
+
+def test_simulate_image_reference_signature_matches_reference_run(gpu):
+    """simulate_image(config, image_seed) -- the reference's own call (scheduler.py:156-183) --
+    with a SimulationConfig-shaped object built from this package's types, against the
+    reference's accumulators for three seeds (tests/golden/sim_config.npz, made by running
+    xtrace.scheduler.simulate_image on test_scheduler.py's small config): per pixel within
+    one f32 ulp of each staged term."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import (BeamSpectrum, CrystalModel, DetectorPanel, Executor, Orientation,
+                                       StructureFactorTable, UnitCell, generate_mosaic_rotations)
+
+    @dataclasses.dataclass
+    class Config:  # the fields and crystal_for_seed of xtrace.io.SimulationConfig (io.py:122-157)
+        cell: UnitCell
+        n_cells: tuple
+        panel: DetectorPanel
+        spectrum: BeamSpectrum
+        sf_table: StructureFactorTable
+        background: BackgroundProfile
+        mosaic_domains: int = 1
+        mosaic_spread_deg: float = 0.0
+        oversample: int = 1
+        thickness_factor: float = 1.0
+
+        def crystal_for_seed(self, seed):
+            mosaic = generate_mosaic_rotations(seed, self.mosaic_spread_deg, self.mosaic_domains)
+            return CrystalModel(cell=self.cell, orientation=Orientation(), n_cells=self.n_cells, mosaic=mosaic,
+                                sf_table=self.sf_table)
+
+    case = np.load(parity.GOLDEN / "sim_config.npz")
+    config = Config(cell=UnitCell(100.0, 100.0, 100.0, 90.0, 90.0, 90.0), n_cells=(5, 5, 5),
+                    panel=DetectorPanel(48, 48, 100e-6, 0.1, (23.5, 23.5)),
+                    spectrum=BeamSpectrum(samples=((1.0, 1.0),), fluence=1e24,
+                                          polarization_on=bool(case["polarization_on"])),
+                    sf_table=StructureFactorTable({}, default_f=100.0),
+                    background=BackgroundProfile(points=((0.0, 2.57), (0.07, 2.8), (0.3, 6.5))),
+                    mosaic_domains=2, mosaic_spread_deg=0.05)
+    with Executor.workers(2) as ex:
+        for seed, want in zip(case["seeds"], case["ref_images"]):
+            got = simulate_image(config, int(seed), ex)
+            assert got.precision == "f64" and got.dims == (48, 48)
+            np.testing.assert_allclose(got.data, want, rtol=2.0 ** -22, atol=0)
+        assert ex.timing_log and ex.timing_log[-1].label == "simulate_image"

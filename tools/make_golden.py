@@ -225,6 +225,27 @@ def stats_case():
             "ref_stats": np.array(rows)}
 
 
+SIM_SEEDS = (11, 12, 13)
+
+
+def sim_config_case():
+    """xtrace.scheduler.simulate_image(config, image_seed) (scheduler.py:156-183) on the
+    reference's own small scheduler config (test_scheduler.py:30-45): the f64 accumulator of
+    spots + background for three image seeds (each seed draws its own mosaic domains)."""
+    import xtrace.io as xio
+    import xtrace.scheduler as xs
+
+    config = xio.SimulationConfig(
+        cell=xm.UnitCell(100.0, 100.0, 100.0, 90.0, 90.0, 90.0), n_cells=(5, 5, 5),
+        panel=xm.DetectorPanel(48, 48, 100e-6, 0.1, (23.5, 23.5)),
+        spectrum=xm.BeamSpectrum(samples=((1.0, 1.0),), fluence=1e24),
+        sf_table=xm.StructureFactorTable({}, default_f=100.0),
+        background=xm.BackgroundProfile(points=((0.0, 2.57), (0.07, 2.8), (0.3, 6.5))),
+        mosaic_domains=2, mosaic_spread_deg=0.05, oversample=1, seed=0)
+    images = np.stack([xs.simulate_image(config, s).data.copy() for s in SIM_SEEDS])
+    return {"seeds": np.array(SIM_SEEDS), "ref_images": images, "polarization_on": config.spectrum.polarization_on}
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
@@ -254,6 +275,11 @@ def main(names):
         np.savez_compressed(OUT / "pipeline_full.npz", ref_image=acc, **{k: np.asarray(v) for k, v in case.items()})
         meta["pipeline_full"] = {"pixels": int(acc.size), "total": float(acc.sum())}
         print("pipeline_full", meta["pipeline_full"], flush=True)
+    if not names or "sim_config" in names:
+        case = sim_config_case()
+        np.savez_compressed(OUT / "sim_config.npz", **case)
+        meta["sim_config"] = {"images": len(SIM_SEEDS), "total": float(case["ref_images"].sum())}
+        print("sim_config", meta["sim_config"], flush=True)
     if not names or "stats" in names:
         case = stats_case()
         np.savez_compressed(OUT / "stats.npz", **case)
