@@ -166,3 +166,21 @@ def test_background_division_identity_is_correctly_rounded():
         r = float(Fraction(x) - Fraction(q0) * Fraction(lam))
         q = float(Fraction(r) * Fraction(inv) + Fraction(q0))
         assert q == x / lam, (x, lam)
+
+
+def test_write_image_bytes_equal_reference(tmp_path):
+    """write_image (io.py:403-434): the .bin payload and the .json sidecar text equal, byte for
+    byte, what the reference's write_image wrote for the same accumulator and metadata
+    (tests/golden/image_io.npz)."""
+    from paper_2205_07976_b200 import BeamSpectrum, DetectorPanel, PixelBuffer
+    from paper_2205_07976_b200.io import read_image, write_image
+
+    case = np.load(parity.GOLDEN / "image_io.npz")
+    panel = DetectorPanel(24, 40, 88.6e-6, 0.1417, (11.5, 19.5))
+    spectrum = BeamSpectrum(samples=((1.7, 0.5), (1.71, 0.25), (1.72, 0.25)), fluence=1e24)
+    path = write_image(PixelBuffer((24, 40), "f64", case["data"]), tmp_path / "img_000007", panel=panel,
+                       spectrum=spectrum, seed=220507983, image_index=7)
+    assert path.read_bytes() == case["bin"].tobytes()
+    assert path.with_suffix(".json").read_text() == str(case["json"])
+    data, side = read_image(path)
+    assert data.shape == (24, 40) and side["image_index"] == 7

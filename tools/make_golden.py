@@ -246,6 +246,25 @@ def sim_config_case():
     return {"seeds": np.array(SIM_SEEDS), "ref_images": images, "polarization_on": config.spectrum.polarization_on}
 
 
+def image_io_case():
+    """xtrace.io.write_image (io.py:403-434) on a seeded f64 accumulator with panel, spectrum,
+    seed and index: the exact .bin bytes and .json text the reference writes."""
+    import tempfile
+
+    import xtrace.io as xio
+
+    rng = np.random.default_rng(7)
+    data = rng.lognormal(0.0, 3.0, 24 * 40)
+    panel = xm.DetectorPanel(24, 40, 88.6e-6, 0.1417, (11.5, 19.5))
+    spectrum = xm.BeamSpectrum(samples=((1.7, 0.5), (1.71, 0.25), (1.72, 0.25)), fluence=1e24)
+    with tempfile.TemporaryDirectory() as d:
+        path = xio.write_image(xk.PixelBuffer((24, 40), "f64", data), Path(d) / "img_000007", panel=panel,
+                               spectrum=spectrum, seed=220507983, image_index=7)
+        bin_bytes = path.read_bytes()
+        json_text = path.with_suffix(".json").read_text()
+    return {"data": data, "bin": np.frombuffer(bin_bytes, dtype=np.uint8), "json": np.array(json_text)}
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
@@ -280,6 +299,11 @@ def main(names):
         np.savez_compressed(OUT / "sim_config.npz", **case)
         meta["sim_config"] = {"images": len(SIM_SEEDS), "total": float(case["ref_images"].sum())}
         print("sim_config", meta["sim_config"], flush=True)
+    if not names or "image_io" in names:
+        case = image_io_case()
+        np.savez_compressed(OUT / "image_io.npz", **case)
+        meta["image_io"] = {"bytes": int(case["bin"].size)}
+        print("image_io", meta["image_io"], flush=True)
     if not names or "stats" in names:
         case = stats_case()
         np.savez_compressed(OUT / "stats.npz", **case)
