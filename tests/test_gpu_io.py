@@ -6,6 +6,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
+import parity
 from paper_2205_07976_b200 import BackgroundProfile, PixelBuffer, simulate_image, synthetic
 from paper_2205_07976_b200 import io as nio
 
@@ -107,3 +108,35 @@ def test_image_stats_and_histogram(gpu):
     assert h.cumulative.tolist() == np.cumsum(h.counts).tolist()
     edge = nio.image_histogram(PixelBuffer((1, 4), "f64", [1.0] * 4), 4, (0.0, 1.0))
     assert edge.counts.tolist() == [0, 0, 0, 4]
+
+
+HIST_SPECS = [(1, (0.0, 1.0)), (3, (0.1, 0.7)), (64, (-2.5, 7.25)), (1000, (1e-3, 3.0))]
+
+
+def hist_values(precision):
+    """tools/make_golden.py:hist_values -- seeded values plus every binning edge case."""
+    rng = np.random.default_rng(42)
+    v = [rng.uniform(-3.0, 8.0, 20000), rng.lognormal(0.0, 1.0, 5000)]
+    for n_bins, (lo, hi) in HIST_SPECS:
+        w = (hi - lo) / n_bins
+        edges = lo + w * np.arange(n_bins + 1)
+        v += [edges, np.nextafter(edges, -np.inf), np.nextafter(edges, np.inf), [lo, hi]]
+    v.append([np.inf, -np.inf, np.nan, 5e-324, -5e-324, 0.0, -0.0])
+    out = np.concatenate([np.asarray(x, dtype=np.float64) for x in v])
+    return out.astype(np.float32) if precision == "f32" else out
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_histogram_equals_reference_run(gpu, precision):
+    """image_histogram against xtrace.kernels.image_histogram's own output
+    (tests/golden/histogram.npz): bin edges, one-ulp neighbours, lo/hi, +-inf, NaN (the
+    reference's int64 cast puts it in bin 0), subnormals -- counts, cumulative, under/overflow
+    exactly equal."""
+    golden = np.load(parity.GOLDEN / "histogram.npz")
+    vals = hist_values(precision)
+    for n_bins, rng_ in HIST_SPECS:
+        h = nio.image_histogram(PixelBuffer((1, vals.size), precision, vals), n_bins, rng_)
+        key = f"{precision}_{n_bins}"
+        assert np.array_equal(h.counts, golden[key + "_counts"]), key
+        assert np.array_equal(h.cumulative, golden[key + "_cumulative"]), key
+        assert [h.underflow, h.overflow] == golden[key + "_under_over"].tolist(), key

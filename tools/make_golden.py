@@ -265,6 +265,37 @@ def image_io_case():
     return {"data": data, "bin": np.frombuffer(bin_bytes, dtype=np.uint8), "json": np.array(json_text)}
 
 
+HIST_SPECS = [(1, (0.0, 1.0)), (3, (0.1, 0.7)), (64, (-2.5, 7.25)), (1000, (1e-3, 3.0))]
+
+
+def hist_values(precision: str) -> np.ndarray:
+    """Seeded values plus every edge case of the binning rule: exact bin edges, lo and hi
+    themselves, neighbours one ulp away, +-inf, NaN, subnormals, signed zeros."""
+    rng = np.random.default_rng(42)
+    v = [rng.uniform(-3.0, 8.0, 20000), rng.lognormal(0.0, 1.0, 5000)]
+    for n_bins, (lo, hi) in HIST_SPECS:
+        w = (hi - lo) / n_bins
+        edges = lo + w * np.arange(n_bins + 1)
+        v += [edges, np.nextafter(edges, -np.inf), np.nextafter(edges, np.inf), [lo, hi]]
+    v.append([np.inf, -np.inf, np.nan, 5e-324, -5e-324, 0.0, -0.0])
+    out = np.concatenate([np.asarray(x, dtype=np.float64) for x in v])
+    return out.astype(np.float32) if precision == "f32" else out
+
+
+def histogram_case():
+    """xtrace.kernels.image_histogram (kernels.py:386-430) on hist_values for every spec."""
+    res = {}
+    for precision in ("f32", "f64"):
+        vals = hist_values(precision)
+        for n_bins, rng_ in HIST_SPECS:
+            h = xk.image_histogram(xk.PixelBuffer((1, vals.size), precision, vals), n_bins, rng_)
+            key = f"{precision}_{n_bins}"
+            res[key + "_counts"] = h.counts
+            res[key + "_cumulative"] = h.cumulative
+            res[key + "_under_over"] = np.array([h.underflow, h.overflow])
+    return res
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
@@ -304,6 +335,11 @@ def main(names):
         np.savez_compressed(OUT / "image_io.npz", **case)
         meta["image_io"] = {"bytes": int(case["bin"].size)}
         print("image_io", meta["image_io"], flush=True)
+    if not names or "histogram" in names:
+        case = histogram_case()
+        np.savez_compressed(OUT / "histogram.npz", **case)
+        meta["histogram"] = {"specs": [list(map(str, x)) for x in HIST_SPECS], "generator": "hist_values"}
+        print("histogram", len(case), flush=True)
     if not names or "stats" in names:
         case = stats_case()
         np.savez_compressed(OUT / "stats.npz", **case)
