@@ -108,13 +108,17 @@ __global__ void __launch_bounds__(kThreads) stats_blocks_kernel(const void* __re
     const int len = (int)min((int64_t)kStatsBlock, n - lo);
     const T* src = static_cast<const T*>(data) + lo;
     double mn = INFINITY, mx = -INFINITY;
+    bool has_nan = false;
     for (int i = threadIdx.x; i < len; i += kThreads) {  // coalesced staging, exact upcast
         const T raw = src[i];
         const double v = (double)raw;
         blk[(i / kLeaf) * kLeafPad + (i % kLeaf)] = raw;
         mn = fmin(mn, v);
         mx = fmax(mx, v);
+        has_nan |= isnan(v);
     }
+    // chunk.min() / chunk.max() propagate NaN (NumPy), fmin/fmax skip it
+    if (__syncthreads_or(has_nan)) mn = mx = NAN;
     mn_s[threadIdx.x] = mn;
     mx_s[threadIdx.x] = mx;
     __syncthreads();
@@ -151,8 +155,10 @@ __global__ void __launch_bounds__(kThreads) stats_blocks_kernel(const void* __re
 // left: T_0 + (T_1 + (... + T_last)).  One block: all segments' tree levels run in
 // parallel in place (global scratch, __syncthreads between levels), then thread 0
 // folds the chain.
+// Python's min(x, y) / max(x, y): y only if it compares below / above x, so a NaN on the
+// left survives and one on the right is dropped -- the reference's semantics, NaN included.
 __device__ __forceinline__ Partial combine_p(const Partial& x, const Partial& y) {  // kernels.py:362-363
-    return Partial{fmin(x.mn, y.mn), fmax(x.mx, y.mx), x.sum + y.sum};
+    return Partial{y.mn < x.mn ? y.mn : x.mn, y.mx > x.mx ? y.mx : x.mx, x.sum + y.sum};
 }
 
 __global__ void __launch_bounds__(1024) stats_final_kernel(Partial* __restrict__ parts, int64_t nb,

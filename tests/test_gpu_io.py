@@ -140,3 +140,40 @@ def test_histogram_equals_reference_run(gpu, precision):
         assert np.array_equal(h.counts, golden[key + "_counts"]), key
         assert np.array_equal(h.cumulative, golden[key + "_cumulative"]), key
         assert [h.underflow, h.overflow] == golden[key + "_under_over"].tolist(), key
+
+
+def stats_special_values():
+    """tools/make_golden.py:stats_special_values (non-finite placements across 5 blocks)."""
+    rng = np.random.default_rng(3)
+    base = rng.uniform(-1.0, 1.0, 5 * 8192 - 100)
+    cases = []
+    for kind, at in (("nan", 5), ("nan", 20000), ("nan", base.size - 1), ("inf", 9000), ("-inf", 30000),
+                     ("nan+inf", (100, 17000)), ("zeros", None)):
+        v = base.copy()
+        if kind == "nan":
+            v[at] = np.nan
+        elif kind == "inf":
+            v[at] = np.inf
+        elif kind == "-inf":
+            v[at] = -np.inf
+        elif kind == "nan+inf":
+            v[at[0]] = np.inf
+            v[at[1]] = np.nan
+        else:
+            v = np.where(np.arange(v.size) % 2 == 0, 0.0, -0.0)
+        cases.append(v)
+    return cases
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_stats_non_finite_semantics_equal_reference_run(gpu, precision):
+    """image_stats with NaN / inf against xtrace.kernels.image_stats's own output
+    (tests/golden/stats_special.npz): NumPy's NaN-propagating block min/max, then Python's
+    min/max along parallel_reduce's tree (a NaN block survives only as a left operand) --
+    min, max, mean, total equal as values (the sign of a zero extremum is not pinned)."""
+    golden = np.load(parity.GOLDEN / "stats_special.npz")[precision]
+    for i, v in enumerate(stats_special_values()):
+        vv = v.astype(np.float32 if precision == "f32" else np.float64)
+        st = nio.image_stats(PixelBuffer((1, vv.size), precision, vv))
+        got = np.array([st.min, st.max, st.mean, st.total])
+        assert np.array_equal(got, golden[i], equal_nan=True), (i, got, golden[i])

@@ -296,6 +296,43 @@ def histogram_case():
     return res
 
 
+def stats_special_values():
+    """Non-finite placements for image_stats: NaN in the first / a middle / the last block,
+    +-inf, NaN with inf, and signed zeros (block length 8192, 5 blocks)."""
+    rng = np.random.default_rng(3)
+    base = rng.uniform(-1.0, 1.0, 5 * 8192 - 100)
+    cases = []
+    for spec in (("nan", 5), ("nan", 20000), ("nan", base.size - 1), ("inf", 9000), ("-inf", 30000),
+                 ("nan+inf", (100, 17000)), ("zeros", None)):
+        v = base.copy()
+        kind, at = spec
+        if kind == "nan":
+            v[at] = np.nan
+        elif kind == "inf":
+            v[at] = np.inf
+        elif kind == "-inf":
+            v[at] = -np.inf
+        elif kind == "nan+inf":
+            v[at[0]] = np.inf
+            v[at[1]] = np.nan
+        else:
+            v = np.where(np.arange(v.size) % 2 == 0, 0.0, -0.0)
+        cases.append(v)
+    return cases
+
+
+def stats_special_case():
+    res = {}
+    for precision in ("f32", "f64"):
+        rows = []
+        for v in stats_special_values():
+            vv = v.astype(np.float32 if precision == "f32" else np.float64)
+            st = xk.image_stats(xk.PixelBuffer((1, vv.size), precision, vv))
+            rows.append([st.min, st.max, st.mean, st.total])
+        res[precision] = np.array(rows)
+    return res
+
+
 def main(names):
     OUT.mkdir(parents=True, exist_ok=True)
     meta = {}
@@ -340,6 +377,11 @@ def main(names):
         np.savez_compressed(OUT / "histogram.npz", **case)
         meta["histogram"] = {"specs": [list(map(str, x)) for x in HIST_SPECS], "generator": "hist_values"}
         print("histogram", len(case), flush=True)
+    if not names or "stats_special" in names:
+        case = stats_special_case()
+        np.savez_compressed(OUT / "stats_special.npz", **case)
+        meta["stats_special"] = {"cases": int(case["f64"].shape[0]), "generator": "stats_special_values"}
+        print("stats_special", case["f64"].tolist(), flush=True)
     if not names or "stats" in names:
         case = stats_case()
         np.savez_compressed(OUT / "stats.npz", **case)
