@@ -800,7 +800,36 @@ static cudaError_t launch_shape(const SpotsParams& P, int shape, size_t smem, cu
 // compute: 0 FP64, 1 FP32 (MUFU numerator), 2 FP32 with the degree-4 (ulp-grade) polynomial,
 // 5 FP32 degree-3 with the polynomial numerator (both sincg only), 4 FP64 with the channel
 // recurrence (sincg only).  idx: Fhkl index kind (kIdxMagic / kIdxWide / kIdxHash).
+// Grid limits: gridDim.z (one slice per panel) and gridDim.y (8-row block lines) are
+// capped at 65535, so very tall panels or very many panels take several launches over
+// row / panel ranges (the kernels index panels through P.panels and rows from P.row0).
+constexpr int kMaxGridYZ = 65535;
+
+template <typename F>
+static cudaError_t for_grid_chunks(const SpotsParams& P, F&& launch) {
+    for (int z0 = 0; z0 < P.n_panels; z0 += kMaxGridYZ) {
+        for (int r0 = P.row0; r0 < P.max_slow; r0 += kMaxGridYZ * kBlockY) {
+            SpotsParams Q = P;
+            Q.panels = P.panels + z0;
+            Q.n_panels = P.n_panels - z0 < kMaxGridYZ ? P.n_panels - z0 : kMaxGridYZ;
+            Q.row0 = r0;
+            Q.max_slow = P.max_slow - r0 < kMaxGridYZ * kBlockY ? P.max_slow : r0 + kMaxGridYZ * kBlockY;
+            const cudaError_t e = launch(Q);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
+
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st) {
+    if (P.n_panels <= kMaxGridYZ && P.max_slow - P.row0 <= kMaxGridYZ * kBlockY)
+        return launch_spots_one(P, compute, shape, idx, st);
+    return for_grid_chunks(P, [&](const SpotsParams& Q) { return launch_spots_one(Q, compute, shape, idx, st); });
+}
+
+static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st) {
     if (compute == 0) {
         const size_t smem = (size_t)P.n_src * 16;
         return idx == kIdxHash ? launch_shape<0, kIdxHash>(P, shape, smem, st)
@@ -829,6 +858,8 @@ static int grid_for(int64_t n, int block) {
 }
 
 cudaError_t launch_background(const SpotsParams& P, cudaStream_t st) {
+    if (P.n_panels > kMaxGridYZ || P.max_slow - P.row0 > kMaxGridYZ * kBlockY)
+        return for_grid_chunks(P, [&](const SpotsParams& Q) { return launch_background(Q, st); });
     dim3 block(kBlockX, kBlockY, 1);
     dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow - P.row0 + kBlockY - 1) / kBlockY, P.n_panels);
     background_kernel<<<grid, block, 0, st>>>(P);

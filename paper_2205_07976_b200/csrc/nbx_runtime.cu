@@ -205,13 +205,10 @@ void check_unit(const double* v, const char* what) {
 
 int64_t count_pixels(const nbx_spots_desc* d) {
     if (!d || d->n_panels < 1 || !d->panels) throw ArgError("descriptor needs at least one panel");
-    // launch geometry limits: one grid z-slice per panel, 8-row block lines on grid y
-    if (d->n_panels > 65535) throw ArgError("at most 65535 panels per launch");
     int64_t n = 0;
     for (int i = 0; i < d->n_panels; ++i) {
         const nbx_panel& p = d->panels[i];
         if (p.slow_pixels < 1 || p.fast_pixels < 1) throw ArgError("panel must have at least one pixel per axis");
-        if (p.slow_pixels > 65535 * 8) throw ArgError("panel has more than 524280 rows");
         n += (int64_t)p.slow_pixels * p.fast_pixels;
     }
     return n;

@@ -688,3 +688,36 @@ def test_c_abi_argument_errors_leave_the_context_usable(gpu):
     again = PixelBuffer.zeros(ctx.panel.dims)
     nanobragg_spots(ctx, again)
     assert np.array_equal(again.data, ref)
+
+
+def test_grid_limits_tall_panel_and_many_panels(gpu):
+    """Beyond one launch's grid (65535 block lines of 8 rows, 65535 panel slices): a 600,000-row
+    panel and a 70,000-panel detector are launched in row / panel chunks -- pieces equal
+    single-panel runs bit for bit."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import Detector
+
+    base = synthetic.roi(synthetic.rayonix_panel(), 1900, 1900, 8, 2)
+    ctx = synthetic.ls49_context(panel=base, n_channels=2, n_domains=1, compute="fp64")
+    tall = dataclasses.replace(base, slow_pixels=600_000)
+    import torch
+
+    from paper_2205_07976_b200 import _native as N
+
+    plan = SpotsPlan(dataclasses.replace(ctx, panel=tall))  # device output: one launch request, row-chunked
+    dev = torch.zeros(plan.n_pixels, dtype=torch.float64, device="cuda")
+    plan.run(dev.data_ptr(), mode=N.OUT_F64, on_device=True)
+    img = dev.cpu().numpy().reshape(600_000, 2)
+    assert np.array_equal(img, run(dataclasses.replace(ctx, panel=tall), "f64").data.reshape(600_000, 2))
+    for r0 in (0, 524_280 - 3, 599_990):
+        piece = dataclasses.replace(base, slow_pixels=8, beam_center=(base.beam_center[0] - r0, base.beam_center[1]))
+        want = run(dataclasses.replace(ctx, panel=piece), "f64").data.reshape(8, 2)
+        assert np.array_equal(img[r0:r0 + 8], want[: min(8, 600_000 - r0)]), r0
+    one = dataclasses.replace(base, slow_pixels=1, fast_pixels=1)
+    panels = tuple(dataclasses.replace(one, beam_center=(base.beam_center[0] + (k % 7), base.beam_center[1]))
+                   for k in range(70_000))
+    many = run(dataclasses.replace(ctx, panel=Detector(panels)), "f64").data
+    for k in (0, 65_534, 65_535, 69_999):
+        want = run(dataclasses.replace(ctx, panel=panels[k]), "f64").data
+        assert many[k] == want[0], k
