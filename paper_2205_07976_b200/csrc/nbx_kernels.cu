@@ -148,6 +148,20 @@ constexpr int kBlockX = 32;
 #define NBX_BLOCK_Y 8
 #endif
 constexpr int kBlockY = NBX_BLOCK_Y;
+// The FP64 recurrence kernel runs 32x4 blocks, 6 per SM (80 registers, 24 warps): +3.5% over
+// 32x8 x 2 (128 registers, 16 warps) -- its loop is latency-limited at 4 warps per scheduler.
+// The FP32 and direct FP64 kernels keep 32x8 (flat / -1.8% with the smaller blocks).
+#ifndef NBX_BLOCK_Y_REC
+#define NBX_BLOCK_Y_REC 4
+#endif
+#ifndef NBX_MIN_BLOCKS_REC
+#define NBX_MIN_BLOCKS_REC 6
+#endif
+template <int COMPUTE>
+constexpr int kBlockYOf = COMPUTE == 2 ? NBX_BLOCK_Y_REC : NBX_BLOCK_Y;
+template <int COMPUTE>
+constexpr int kMinBlocksOf = COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : (COMPUTE == 2 ? NBX_MIN_BLOCKS_REC : NBX_MIN_BLOCKS_F64);
+constexpr int kBlockYMin = NBX_BLOCK_Y_REC < NBX_BLOCK_Y ? NBX_BLOCK_Y_REC : NBX_BLOCK_Y;
 constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
 constexpr int kPolyF64 = 6;  // FP64 Q(s) degree (rel err 1.2e-13)
 constexpr int kNewtonF64 = 1;
@@ -548,31 +562,32 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
 // the channel recurrence (sincg only).
 // ---------------------------------------------------------------------------
 template <int COMPUTE, int SHAPE, int IDX, int PDEG>
-__global__ void __launch_bounds__(kBlockX* kBlockY, COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : NBX_MIN_BLOCKS_F64) spots_kernel(const SpotsParams P) {
+__global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMPUTE>) spots_kernel(const SpotsParams P) {
+    constexpr int kBY = kBlockYOf<COMPUTE>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.y * kBlockX + threadIdx.x;
     if constexpr (COMPUTE == 1) {
         ChunkF32* k = reinterpret_cast<ChunkF32*>(smem_raw);
-        for (int i = tid; i < P.n_chunks; i += kBlockX * kBlockY) k[i] = P.chunks[i];
+        for (int i = tid; i < P.n_chunks; i += kBlockX * kBY) k[i] = P.chunks[i];
         float4* s = reinterpret_cast<float4*>(smem_raw + 16 * P.n_chunks);
         const float4* g = static_cast<const float4*>(P.chan);
-        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];  // FP32: n_src counts pairs
+        for (int i = tid; i < P.n_src; i += kBlockX * kBY) s[i] = g[i];  // FP32: n_src counts pairs
     } else {
         double2* s = reinterpret_cast<double2*>(smem_raw);
         const double2* g = static_cast<const double2*>(P.chan);
-        for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) s[i] = g[i];
+        for (int i = tid; i < P.n_src; i += kBlockX * kBY) s[i] = g[i];
         if constexpr (COMPUTE == 2) {
             RunF64* r = reinterpret_cast<RunF64*>(smem_raw + 16 * P.n_src);
-            for (int i = tid; i < P.n_runs; i += kBlockX * kBlockY) r[i] = P.runs[i];
+            for (int i = tid; i < P.n_runs; i += kBlockX * kBY) r[i] = P.runs[i];
             float* v = reinterpret_cast<float*>(smem_raw + 16 * P.n_src + sizeof(RunF64) * P.n_runs);
-            for (int i = tid; i < P.n_src; i += kBlockX * kBlockY) v[i] = __double2float_rn(g[i].x);
+            for (int i = tid; i < P.n_src; i += kBlockX * kBY) v[i] = __double2float_rn(g[i].x);
         }
     }
     __syncthreads();
 
     const DevPanel& pan = P.panels[blockIdx.z];
     const int f = blockIdx.x * kBlockX + threadIdx.x;
-    const int sl = P.row0 + blockIdx.y * kBlockY + threadIdx.y;
+    const int sl = P.row0 + blockIdx.y * kBY + threadIdx.y;
     if (sl >= pan.slow || sl >= P.max_slow || f >= pan.fast) return;
 
     const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
@@ -781,8 +796,9 @@ static cudaError_t launch_t(const SpotsParams& P, size_t smem, cudaStream_t st) 
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    dim3 block(kBlockX, kBlockY, 1);
-    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow - P.row0 + kBlockY - 1) / kBlockY, P.n_panels);
+    constexpr int kBY = kBlockYOf<COMPUTE>;
+    dim3 block(kBlockX, kBY, 1);
+    dim3 grid((P.max_fast + kBlockX - 1) / kBlockX, (P.max_slow - P.row0 + kBY - 1) / kBY, P.n_panels);
     k<<<grid, block, smem, st>>>(P);
     return cudaGetLastError();
 }
@@ -808,12 +824,12 @@ constexpr int kMaxGridYZ = 65535;
 template <typename F>
 static cudaError_t for_grid_chunks(const SpotsParams& P, F&& launch) {
     for (int z0 = 0; z0 < P.n_panels; z0 += kMaxGridYZ) {
-        for (int r0 = P.row0; r0 < P.max_slow; r0 += kMaxGridYZ * kBlockY) {
+        for (int r0 = P.row0; r0 < P.max_slow; r0 += kMaxGridYZ * kBlockYMin) {
             SpotsParams Q = P;
             Q.panels = P.panels + z0;
             Q.n_panels = P.n_panels - z0 < kMaxGridYZ ? P.n_panels - z0 : kMaxGridYZ;
             Q.row0 = r0;
-            Q.max_slow = P.max_slow - r0 < kMaxGridYZ * kBlockY ? P.max_slow : r0 + kMaxGridYZ * kBlockY;
+            Q.max_slow = P.max_slow - r0 < kMaxGridYZ * kBlockYMin ? P.max_slow : r0 + kMaxGridYZ * kBlockYMin;
             const cudaError_t e = launch(Q);
             if (e != cudaSuccess) return e;
         }
@@ -824,7 +840,7 @@ static cudaError_t for_grid_chunks(const SpotsParams& P, F&& launch) {
 static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
 
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st) {
-    if (P.n_panels <= kMaxGridYZ && P.max_slow - P.row0 <= kMaxGridYZ * kBlockY)
+    if (P.n_panels <= kMaxGridYZ && P.max_slow - P.row0 <= kMaxGridYZ * kBlockYMin)
         return launch_spots_one(P, compute, shape, idx, st);
     return for_grid_chunks(P, [&](const SpotsParams& Q) { return launch_spots_one(Q, compute, shape, idx, st); });
 }
