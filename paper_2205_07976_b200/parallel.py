@@ -21,7 +21,6 @@ from __future__ import annotations
 
 from typing import Callable
 
-import numpy as np
 
 from .kernels import PixelBuffer, SpotsContext, SpotsPlan
 from . import _native as N

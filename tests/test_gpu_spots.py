@@ -5,7 +5,6 @@ on total and per-spot intensity; FP32 path 1e-4.  Extensions without a
 reference (thickness, shapes, phi, multi-panel, channel shards) are checked
 against the CPU oracle (oracle/) at the FP64 tolerance.
 """
-import math
 
 import numpy as np
 import pytest

@@ -7,10 +7,9 @@ import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np
 import torch
 
-from paper_2205_07976_b200 import BackgroundProfile, PixelBuffer, SpotsPlan, add_background, simulate_image, synthetic
+from paper_2205_07976_b200 import BackgroundProfile, PixelBuffer, SpotsPlan, simulate_image, synthetic
 from paper_2205_07976_b200 import _native as N
 from paper_2205_07976_b200.kernels import _bg_descriptor
 

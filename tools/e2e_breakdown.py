@@ -4,7 +4,6 @@ import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np
 import torch
 
 from paper_2205_07976_b200 import PixelBuffer, SpotsPlan, describe, nanobragg_spots, synthetic

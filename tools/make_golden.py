@@ -28,7 +28,6 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import xtrace.kernels as xk  # noqa: E402
 import xtrace.model as xm  # noqa: E402
 
-from paper_2205_07976_b200 import model as mm  # noqa: E402
 from paper_2205_07976_b200 import synthetic as syn  # noqa: E402
 
 OUT = ROOT / "tests" / "golden"

@@ -15,7 +15,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 
-from paper_2205_07976_b200 import (BackgroundProfile, Detector, PixelBuffer, SpotsPlan, add_array, add_noise,
+from paper_2205_07976_b200 import (BackgroundProfile, PixelBuffer, SpotsPlan, add_array, add_noise,
                                    nanobragg_spots, simulate_image, synthetic)
 from paper_2205_07976_b200 import _native as N
 from paper_2205_07976_b200.io import image_histogram, image_stats
