@@ -326,8 +326,9 @@ def run_ours(args):
                    "l2": "256 MB buffer written between timed images (L2 flushed); Fhkl grid L2-resident by design"},
         "gsteps_per_s": gsteps,
         "kernel_ms_mean": mean_kernel,
-        # one spot kernel per image per rank (+ one finalize on rank 0 in channel mode); the flush is torch's
-        "gpu_launches": args.steps * (2 if (mode == "channels" and rank == 0) else 1),
+        # whole job: one spot kernel per step on every rank (+ one finalize / slot reduction per
+        # step on the root in channel mode); the L2 flush is torch's, not counted
+        "gpu_launches": args.steps * world + (args.steps if mode == "channels" else 0),
         "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
                      "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
                      "traffic": traffic,

@@ -31,7 +31,7 @@ def torchrun(args, port):
 def test_image_sharded_two_ranks(gpu):
     d = torchrun(["--steps", "2", "--warmup", "3", "--size", "512", "--no-extras"], 29531)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["global_batch"] == 2
-    assert d["value"] > 0 and d["gpu_launches"] == 2
+    assert d["value"] > 0 and d["gpu_launches"] == 2 * 2  # whole job: 2 steps x 2 ranks
 
 
 @pytest.mark.parametrize("transport", ["nccl", "p2p"])
@@ -40,6 +40,7 @@ def test_channel_sharded_two_ranks(gpu, transport):
                   "--transport", transport], 29532 if transport == "nccl" else 29536)
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["images_per_gpu_per_step"] == 0.5
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] == 2 * 2 + 2  # 2 steps x 2 ranks + one root reduction per step
 
 
 CAMPAIGN_SCRIPT = r'''
