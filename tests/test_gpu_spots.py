@@ -720,3 +720,38 @@ def test_grid_limits_tall_panel_and_many_panels(gpu):
     for k in (0, 65_534, 65_535, 69_999):
         want = run(dataclasses.replace(ctx, panel=panels[k]), "f64").data
         assert many[k] == want[0], k
+
+
+def test_caller_stream_and_probe(gpu):
+    """nbx_ctx_set_stream: launches go to the caller's stream (a torch stream here) with the same
+    image; NULL restores the context's own stream.  nbx_ctx_synchronize and the FMA-peak probe
+    the bench's roofline uses answer sensibly."""
+    import torch
+
+    from paper_2205_07976_b200 import _native as N
+
+    cx = N.context()
+    ctx = synthetic.ls49_context(panel=synthetic.roi(synthetic.rayonix_panel(), 1800, 1800, 40, 64), n_channels=8,
+                                 n_domains=2, compute="fp32")
+    plan = SpotsPlan(ctx)
+    a = torch.zeros(plan.n_pixels, dtype=torch.float32, device="cuda")
+    plan.run(a.data_ptr(), on_device=True)
+    s = torch.cuda.Stream()
+    b = torch.zeros_like(a)
+    with cx.lock:
+        assert cx.lib.nbx_ctx_set_stream(cx.handle, N.C.c_void_p(s.cuda_stream)) == N.NBX_OK
+    try:
+        plan.run(b.data_ptr(), on_device=True)
+        s.synchronize()
+        assert torch.equal(a, b)
+        with cx.lock:
+            assert cx.lib.nbx_ctx_synchronize(cx.handle) == N.NBX_OK
+    finally:
+        with cx.lock:
+            assert cx.lib.nbx_ctx_set_stream(cx.handle, None) == N.NBX_OK
+    plan.close()
+    for fp64, floor in ((0, 20.0), (1, 10.0)):
+        tf = N.C.c_double(0.0)
+        with cx.lock:
+            assert cx.lib.nbx_probe_fma_peak(cx.handle, fp64, N.C.byref(tf)) == N.NBX_OK
+        assert floor < tf.value < 200.0, (fp64, tf.value)
