@@ -488,14 +488,15 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
         if (plan->kernel_variant == 1 && d->shape == NBX_SHAPE_SINCG) {
             // MUFU.SIN's ~1e-6 absolute error averages out over the many (channel, domain,
             // sub-pixel) samples of a pixel; with few samples per pixel (the C1 toy: one
-            // channel x one domain, side lobes sampled one point per pixel) take the
-            // polynomial numerator instead.  NBX_FP32_NUM=mufu|poly forces either.
+            // channel x one domain, side lobes sampled one point per pixel) nothing averages,
+            // and such images are small: take the degree-4 polynomial loop (variant 2, worst
+            // golden margin 83x instead of 9.8x for degree 3).  NBX_FP32_NUM=mufu|poly forces
+            // the MUFU loop or the degree-3 polynomial loop (variant 5).
             const char* nev = std::getenv("NBX_FP32_NUM");
             const double per_pixel = off > 0 ? (double)plan->steps / (double)off : 0.0;
-            bool poly = per_pixel < 256.0;
-            if (nev && std::strcmp(nev, "mufu") == 0) poly = false;
-            if (nev && std::strcmp(nev, "poly") == 0) poly = true;
-            if (poly) plan->kernel_variant = 5;
+            if (per_pixel < 256.0) plan->kernel_variant = 2;
+            if (nev && std::strcmp(nev, "mufu") == 0) plan->kernel_variant = 1;
+            if (nev && std::strcmp(nev, "poly") == 0) plan->kernel_variant = 5;
         }
         plan->uniform_panels = true;
         for (const auto& q : hp) plan->uniform_panels &= (q.slow == max_slow && q.fast == max_fast);
