@@ -39,6 +39,9 @@ for compute in ("fp32", "fp64"):
 os.environ["NBX_FP32_POLY"] = "4"
 run(synthetic.ls49_context(panel=roi, n_channels=8, n_domains=2, compute="fp32"))
 del os.environ["NBX_FP32_POLY"]
+os.environ["NBX_FP32_NUM"] = "poly"  # the degree-3 polynomial loop (variant 5)
+run(synthetic.ls49_context(panel=roi, n_channels=8, n_domains=2, compute="fp32"))
+del os.environ["NBX_FP32_NUM"]
 for shape in ("gauss", "round", "tophat"):
     for compute in ("fp32", "fp64"):
         run(dataclasses.replace(synthetic.ls49_context(panel=roi, n_channels=4, n_domains=2, compute=compute),
