@@ -516,7 +516,8 @@ def cpu_baseline_port(ctx, panel, steps_per_image, oracle):
 
     per_pixel = steps_per_image // panel.n_pixels  # every pixel costs the same number of steps
     one = panel.panels[0] if hasattr(panel, "panels") and len(panel.panels) > 1 else panel
-    rows = 16 if per_pixel <= 10000 else 4
+    # ~1.6e9 steps: about 10 s of CPU work on the box's 16 host cores, whatever the config
+    rows = max(1, min(one.slow_pixels, round(1.6e9 / (one.fast_pixels * per_pixel))))
     r0 = one.slow_pixels // 2 - rows // 2
     sub = dataclasses.replace(ctx, panel=synthetic.roi(one, r0, 0, rows, one.fast_pixels))
     desc = describe(sub)
