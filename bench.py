@@ -37,7 +37,8 @@ STEP_INSTR = 126  # FP-pipe instructions per step, SURVEY §8 D1 (FMA = 1)
 # What the implementation actually issues per step on its bounding pipe, counted in the
 # SASS of the hot loop (tools/sass_loop.py), by nbx_plan_info_t.kernel_variant:
 #   (pipe, pipe lane-ops per step, lanes per SM per clock of that pipe)
-IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 22, 64)}
+IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 22, 64),
+            6: ("fp64", 21, 64)}
 SMS = 148
 
 
@@ -47,7 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--compute", default="fp32", choices=["fp32", "fp64"])
+    # fp64 = the reference's own arithmetic (kernels.py:247-273 computes in float64) and the drop-in's
+    # default for a reference SpotsContext: the headline.  fp32 is reported beside it (fp32_path).
+    ap.add_argument("--compute", default="fp64", choices=["fp32", "fp64"])
     ap.add_argument("--size", type=int, default=3840)
     ap.add_argument("--channels", type=int, default=100)
     ap.add_argument("--domains", type=int, default=50)
@@ -294,14 +297,6 @@ def run_ours(args):
     value = total_images / (elapsed / 1e3)
     gsteps = total_images * steps_per_image / (elapsed / 1e3) / 1e9
     mean_kernel = statistics.fmean(kernel_ms)
-    achieved = STEP_INSTR * 2.0 * steps_per_unit / (mean_kernel / 1e3) / 1e12
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get(f"spots_{args.compute}", {}).get("dram_bytes_per_launch")
-        except (ValueError, AttributeError):
-            traffic = None
     workload = {"image": WORKLOAD if size == 3840 else f"{WORKLOAD} (ROI {size}x{size})",
                 "channels": f"C5 single LS49-shape image, {size}x{size}, {args.channels} channels (7020 + 0.2 j eV), "
                             f"{args.domains} mosaic domains, channel-sharded over {world} GPU(s) + "
@@ -329,27 +324,10 @@ def run_ours(args):
         # whole job: one spot kernel per step on every rank (+ one finalize / slot reduction per
         # step on the root in channel mode); the L2 flush is torch's, not counted
         "gpu_launches": args.steps * world + (args.steps if mode == "channels" else 0),
-        "roofline": {"bound": "fp32_pipe" if args.compute == "fp32" else "fp64_pipe", "achieved": achieved,
-                     "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
-                     "traffic": traffic,
-                     "traffic_note": "ncu dram read+write bytes of one spot launch (profiles/ncu_summary.json): "
-                                     "reads are the L2-resident inputs once; most of the image write-back is "
-                                     "still in the 126 MB L2 when the kernel ends, so traffic < writeback bytes",
-                     # the image write-back (the path's only HBM stream; north_star asks for it)
-                     "writeback": {"bytes_per_image": int(plans[0].n_pixels) * 4,
-                                   "gbs": plans[0].n_pixels * 4 / (mean_kernel / 1e3) / 1e9},
-                     "basis": f"{STEP_INSTR} FP-pipe instr/step x 2 FLOP x steps / mean spot-kernel time; "
-                              "peak = live FMA probe (nbx_probe_fma_peak) on this GPU"},
         "clocks": clocks.summary(),
     }
-    # the implementation's own pipe utilisation (frac above is against the fixed 126-op figure)
-    pipe, ops, lanes = IMPL_OPS.get(plans[0].info.kernel_variant, (None, None, None))
     clk = result["clocks"].get("sm_mhz") or 1965.0
-    if ops:
-        result["roofline"]["implementation"] = {
-            "kernel_variant": plans[0].info.kernel_variant, "pipe": pipe, "pipe_ops_per_step": ops,
-            "pipe_frac": gsteps / world * 1e9 * ops / (SMS * lanes * clk * 1e6),
-            "basis": "steps/s x SASS-counted bounding-pipe lane-ops per step / (148 SMs x lanes x SM clock)"}
+    result["roofline"] = roofline(plans[0], mean_kernel, peak.value, clk, args.compute, plans[0].n_pixels * 4)
 
     if not args.no_extras:
         # e2e: the public API with host buffers, descriptor upload and image download inside the timed region
@@ -390,23 +368,37 @@ def run_ours(args):
                          "note": "whole job: every rank simulates its own images, slowest rank's time" if
                          mode != "channels" and world > 1 else "whole job", "call_wall_ms": call_ms}
 
-    if rank == 0 and not args.no_extras and mode == "image" and args.compute == "fp32":
-        # FP64 path on the same workload (the 1e-9 parity path)
-        p64 = SpotsPlan(ctx_for(0, "fp64"), device=local)
-        p64.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
-        ms64 = []
-        for _ in range(2):
+    if rank == 0 and not args.no_extras and mode == "image":
+        # the other compute path on the same workload (FP32: the 1e-4 path; FP64: the 1e-9 path), kernel time,
+        # roofline and its own e2e through nanobragg_spots with host buffers
+        other = "fp32" if args.compute == "fp64" else "fp64"
+        po = SpotsPlan(ctx_for(0, other), device=local)
+        po.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+        mso = []
+        for _ in range(3):
             flush.zero_()
-            p64.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
-            ms64.append(p64.kernel_ms)
-        peak64 = N.C.c_double(0.0)
-        cx.lib.nbx_probe_fma_peak(cx.handle, 1, N.C.byref(peak64))
-        ach64 = STEP_INSTR * 2.0 * p64.steps / (statistics.fmean(ms64) / 1e3) / 1e12
-        result["fp64_path"] = {"kernel_ms": statistics.fmean(ms64),
-                               "gsteps_per_s": p64.steps / statistics.fmean(ms64) / 1e6,
-                               "roofline": {"bound": "fp64_pipe", "achieved": ach64, "peak": peak64.value,
-                                            "unit": "TFLOP/s", "frac": ach64 / peak64.value if peak64.value else None}}
-        p64.close()
+            po.run(out.data_ptr(), mode=N.OUT_F32, on_device=True)
+            mso.append(po.kernel_ms)
+        peak_o = N.C.c_double(0.0)
+        cx.lib.nbx_probe_fma_peak(cx.handle, 1 if other == "fp64" else 0, N.C.byref(peak_o))
+        ko = statistics.fmean(mso)
+        block = {"dtype": "f64" if other == "fp64" else "f32", "kernel_ms": ko, "images_per_s": 1e3 / ko,
+                 "gsteps_per_s": po.steps / ko / 1e6,
+                 "roofline": roofline(po, ko, peak_o.value, clk, other, po.n_pixels * 4)}
+        po.close()
+        octx = [ctx_for(2000 + i, other) for i in range(3)]
+        img_o = PixelBuffer.zeros(panel.dims, "f32")
+        nanobragg_spots(octx[0], img_o)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for c in octx[1:]:
+            nanobragg_spots(c, img_o)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e2e_o = ev0.elapsed_time(ev1) / (len(octx) - 1)
+        block["e2e"] = {"value": 1e3 / e2e_o, "unit": "images/s", "ms_per_step": e2e_o,
+                        "api": "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"}
+        result[f"{other}_path"] = block
 
     if rank == 0 and not args.no_extras and world == 1 and mode == "image":
         result["stages"] = stage_timings(cx, N, torch, stream, ctx_for(0, args.compute), panel)
@@ -420,6 +412,50 @@ def run_ours(args):
         p.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline(plan, kernel_ms: float, peak_tflops: float, clk_mhz: float, compute: str, writeback_bytes: int) -> dict:
+    """Roofline of the spot kernel on its bounding pipe.
+
+    achieved = SASS-counted bounding-pipe lane-ops per step (the channel loop of the kernel variant,
+    tools/sass_loop.py; per-run anchors and per-segment events excluded, so this under-counts) x steps /
+    kernel time, as TFLOP/s with one pipe op = 2 FLOP (the FMA convention of the peak); peak = the live
+    FMA probe of the same pipe on this GPU (MEASURED_PEAKS.json holds no FP32/FP64 figure); frac =
+    achieved / peak.  d1_frac keeps SURVEY §8 D1's fixed 126 instructions per step (it exceeds 1:
+    the implementation needs far fewer instructions per step than that nominal count).
+    """
+    variant = plan.info.kernel_variant
+    pipe, ops, lanes = IMPL_OPS.get(variant, ("fp64" if compute == "fp64" else "fma", STEP_INSTR, 64))
+    sps = plan.steps / (kernel_ms / 1e3)
+    achieved = 2.0 * ops * sps / 1e12
+    d1 = 2.0 * STEP_INSTR * sps / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    ncu_pipe = None
+    if prof.exists():
+        try:
+            rec = json.loads(prof.read_text()).get(f"spots_{compute}", {})
+            traffic = rec.get("dram_bytes_per_launch")
+            ncu_pipe = rec.get("pipes_pct", {}).get("cycles_fp64" if compute == "fp64" else "cycles_fma")
+        except (ValueError, AttributeError):
+            traffic = None
+    return {
+        "bound": "fp64_pipe" if pipe == "fp64" else "fp32_fma_pipe", "achieved": achieved, "peak": peak_tflops,
+        "unit": "TFLOP/s", "frac": achieved / peak_tflops if peak_tflops else None, "traffic": traffic,
+        "kernel_variant": variant, "pipe_ops_per_step": ops,
+        "pipe_frac_nominal": sps * ops / (SMS * lanes * clk_mhz * 1e6),
+        "ncu_pipe_active_pct": ncu_pipe,
+        "d1_frac": d1 / peak_tflops if peak_tflops else None, "d1_instr_per_step": STEP_INSTR,
+        "basis": f"{ops} SASS-counted {pipe}-pipe ops per step in the channel loop (kernel variant {variant}) x "
+                 f"steps / mean spot-kernel time (CUDA events), 1 op = 2 FLOP; peak = live {pipe} FMA probe "
+                 "(nbx_probe_fma_peak) on this GPU; pipe_frac_nominal uses 148 SMs x lanes/SM x median SM clock; "
+                 "ncu_pipe_active_pct = sm__pipe_" + ("fp64" if pipe == "fp64" else "fma") +
+                 "_cycles_active of the committed capture (profiles/ncu_summary.json)",
+        "traffic_note": "ncu dram read+write bytes of one spot launch (profiles/ncu_summary.json): the inputs are "
+                        "read once (L2-resident); most of the image write-back is still in the 126 MB L2 when "
+                        "the kernel ends, so traffic < write-back bytes",
+        "writeback": {"bytes_per_image": int(writeback_bytes), "gbs": writeback_bytes / (kernel_ms / 1e3) / 1e9},
+    }
 
 
 def hbm_peak_gbs() -> tuple[float, str]:

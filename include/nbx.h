@@ -140,7 +140,8 @@ typedef struct nbx_plan_info_t {
     double scale;                /* r_e^2 * fluence / norm */
     int32_t channel_runs;        /* FP64 path: uniform 1/lambda runs evaluated by the channel
                                     recurrence (0: direct per-channel evaluation) */
-    int32_t kernel_variant;      /* 0 FP64 direct, 4 FP64 recurrence, 1 FP32 MUFU numerator,
+    int32_t kernel_variant;      /* 0 FP64 direct, 6 FP64 segmented recurrence, 4 FP64 bracket
+                                    recurrence (NBX_FP64_REC=1), 1 FP32 MUFU numerator,
                                     5 FP32 polynomial numerator, 2 FP32 degree-4 polynomial */
 } nbx_plan_info_t;
 

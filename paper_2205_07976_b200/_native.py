@@ -252,12 +252,18 @@ class Descriptor:
         return sum(int(p.slow_pixels) * int(p.fast_pixels) for p in self._panels)
 
 
-def check(ctx: Context, status: int, first_bad: int = -1, label: str = "nanobragg_spots"):
-    """Translate an NBX status into the reference's exceptions."""
-    from .errors import NumericalFault, PatternFault, ShapeMismatchError
+def check(ctx: Context, status: int, first_bad: int = -1, label: str = "nanobragg_spots", errors=None):
+    """Translate an NBX status into the reference's exceptions.
 
+    ``errors`` is the module whose classes are raised (``errors.hierarchy_for``: the
+    reference's own ``xtrace.errors`` when the call came with xtrace objects).
+    """
     if status == NBX_OK:
         return
+    if errors is None:
+        from . import errors
+    NumericalFault, PatternFault, ShapeMismatchError = (errors.NumericalFault, errors.PatternFault,
+                                                        errors.ShapeMismatchError)
     msg = ctx.error()
     if status == NBX_ERR_NUMERICAL:
         if label == "simulate_image":  # which stage of the fused image faulted

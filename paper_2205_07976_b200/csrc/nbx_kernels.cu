@@ -157,10 +157,19 @@ constexpr int kBlockY = NBX_BLOCK_Y;
 #ifndef NBX_MIN_BLOCKS_REC
 #define NBX_MIN_BLOCKS_REC 6
 #endif
+#ifndef NBX_BLOCK_Y_SEG
+#define NBX_BLOCK_Y_SEG 4
+#endif
+#ifndef NBX_MIN_BLOCKS_SEG
+#define NBX_MIN_BLOCKS_SEG 5
+#endif
 template <int COMPUTE>
-constexpr int kBlockYOf = COMPUTE == 2 ? NBX_BLOCK_Y_REC : NBX_BLOCK_Y;
+constexpr int kBlockYOf = COMPUTE == 2 ? NBX_BLOCK_Y_REC : (COMPUTE == 3 ? NBX_BLOCK_Y_SEG : NBX_BLOCK_Y);
 template <int COMPUTE>
-constexpr int kMinBlocksOf = COMPUTE == 1 ? NBX_MIN_BLOCKS_F32 : (COMPUTE == 2 ? NBX_MIN_BLOCKS_REC : NBX_MIN_BLOCKS_F64);
+constexpr int kMinBlocksOf = COMPUTE == 1   ? NBX_MIN_BLOCKS_F32
+                             : COMPUTE == 2 ? NBX_MIN_BLOCKS_REC
+                             : COMPUTE == 3 ? NBX_MIN_BLOCKS_SEG
+                                            : NBX_MIN_BLOCKS_F64;
 constexpr int kBlockYMin = NBX_BLOCK_Y_REC < NBX_BLOCK_Y ? NBX_BLOCK_Y_REC : NBX_BLOCK_Y;
 constexpr int kPolyF32 = 3;  // FP32 Q(s) degree (4 = the ulp-grade variant, NBX_FP32_POLY=4)
 constexpr int kPolyF64 = 6;  // FP64 Q(s) degree (rel err 1.2e-13)
@@ -558,8 +567,190 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
 }
 
 // ---------------------------------------------------------------------------
+// FP64 path, SEGMENTED channel recurrence (COMPUTE 3, the default for uniform
+// runs).  Same sine sequences as above, but the per-channel bookkeeping of the
+// bracket variant -- the Fhkl index and gather, the small-denominator test --
+// leaves the channel loop.  Along a run the exact phase of each axis is linear
+// in the channel number,
+//     h_{b+j} = h_b + j Delta,   Delta = S delta     (to < 1e-12: host-checked run)
+// and the host cuts runs so that |Delta| (len - 1) <= 0.9 for every reachable S.
+// From ONE exact evaluation at the run's first channel b (h = S (1/lambda_b), the
+// reference's half-away index n and t = h - n, kernels.py:145-146,257-268), with
+// v = sign(Delta) t in [-1/2, 1/2] and a = |Delta|, the phase v + j a of every
+// channel of the run lies in [-1/2, 1.4]; so per axis, per run:
+//   * the index changes at most once: n -> n + sign(Delta) at the first channel with
+//     v + j a >= 1/2 + kSegMargin (the CROSSING channel);
+//   * channels with |v + j a - z| < rho for z in {-1/2, 1/2} (rho = kSegMargin:
+//     the index is not provably n or n + sign) or z in {0, 1} (rho = kSegThr +
+//     kSegMargin: |sin(pi h)| < ~1e-4, the Bragg-peak centre where the recurrence's
+//     ~1e-14 absolute drift would matter, and the reference's limit branch at t == 0)
+//     are SLOW channels, evaluated directly from the exact reduced phase (axis_f64).
+// These channel numbers are computed in FP32 (relative error ~4e-7: < 1e-6 of phase,
+// inside the 2e-6 margin).  The channel loop then only compares k with the next
+// event: at a crossing the segment sum is flushed (acc += F^2 seg) and F^2 switches
+// to the value prefetched for the next segment (its gather's latency hides behind the
+// channels before the crossing); at a slow channel the exact value goes straight
+// into acc.  Per channel: the sines' products, one reciprocal, seg += w (nn/dd)^2 and
+// the recurrences -- 21 FP64 ops, no index arithmetic, no gather.
+//
+// Anchors use the reduced-argument polynomial x Q(x^2) = sin(pi x)/pi (|x| <= 0.52,
+// degree 7, rel err 2.9e-16) instead of sincospi: the sequences carry
+// sin(pi h)/pi (the common 1/pi cancels in the ratio), and Reinsch's start
+//     s_0 = sin(pi x0)/pi,  d_0 = s_0 - s_{-1} = (2/pi) cos(pi (x0 - u)) sin(pi u),
+//     alpha = 4 sin^2(pi u),  u = y/2,  |u| <= 1/4,
+// with cos(pi z) = sin(pi (1/2 - |z|)) for |z| <= 3/4, is three polynomials and no
+// range reduction beyond one rint per argument.
+// ---------------------------------------------------------------------------
+constexpr float kSegThr = 3.2e-5f;      // |t| below this: the channel is evaluated directly
+constexpr float kSegMargin = 2e-6f;     // FP32 prediction margin (phase units)
+constexpr int kSegNone = 0x3FFFFFFF;
+constexpr double kPi = 3.14159265358979323846;
+
+// sin(pi x)/pi for |x| <= 0.52 (degree-7 Q, rel err 2.9e-16)
+__device__ __forceinline__ double sinpi_over_pi(double x) { return x * q_sinpi_f64<7>(x * x); }
+
+// The scaled sequence s_k = sin(pi (x0 + k y))/pi (up to a sign flip per step), |x0| <= 1/2.
+__device__ __forceinline__ SineSeq sine_seq_poly(double x0, double y) {
+    y -= rint(y);                                   // |y| <= 1/2: sin^2 has period 1
+    const double u = 0.5 * y;                       // |u| <= 1/4
+    SineSeq q;
+    q.s = sinpi_over_pi(x0);
+    const double uq = sinpi_over_pi(u);             // sin(pi u)/pi
+    const double w = 0.5 - fabs(x0 - u);            // cos(pi z) = sin(pi w), |w| <= 1/2
+    const double wq = sinpi_over_pi(w);             // cos(pi z)/pi
+    q.d = (2.0 * kPi) * wq * uq;                    // (2/pi) cos(pi z) sin(pi u)
+    const double a2 = (2.0 * kPi) * uq;             // 2 sin(pi u)
+    q.a = a2 * a2;                                  // 4 sin^2(pi u)
+    return q;
+}
+
+struct AxisSeg {
+    SineSeq den, num;
+    float v, invd;  // signed phase sign(Delta) t at the run's first channel, 1/|Delta|
+    int n, dn;      // reference index at the first channel, its step at the crossing (+-1)
+    int c;          // run-relative crossing channel (kSegNone: none in the run)
+};
+
+// Exact state of one axis at the run's first channel (1/lambda = iv) and its sequences.
+__device__ __forceinline__ AxisSeg axis_seg(double S, double iv, double delta, double N, int len) {
+    AxisSeg a;
+    const double h = S * iv;                        // kernels.py:257-260
+    const double n = round_half_away(h);            // kernels.py:145-146
+    const double t = h - n;                         // exact
+    const double d = S * delta;                     // raw phase step per channel
+    a.den = sine_seq_poly(t, d);
+    const double nt = N * t;                        // N n is an integer
+    a.num = sine_seq_poly(nt - rint(nt), N * d);
+    const float df = __double2float_rn(d);
+    const float tf = __double2float_rn(t);
+    a.n = __double2int_rn(n);
+    a.dn = df < 0.0f ? -1 : 1;
+    a.v = df < 0.0f ? -tf : tf;
+    a.invd = 1.0f / fmaxf(fabsf(df), 1e-30f);
+    const float c = ceilf((0.5f + kSegMargin - a.v) * a.invd);  // first channel surely past 1/2
+    a.c = c < (float)len ? (int)c : kSegNone;
+    return a;
+}
+
+// First run-relative channel j >= j0 with |v + j |Delta| - z| < rho (as a float; 3e38: none).
+__device__ __forceinline__ float seg_first_in(float j0, float v, float invd, float z, float rho) {
+    const float lo = (z - rho - v) * invd, hi = (z + rho - v) * invd;
+    const float f = fmaxf(j0, floorf(lo) + 1.0f);
+    return f < hi ? f : 3.0e38f;
+}
+
+__device__ __forceinline__ float seg_slow_axis(float j0, float v, float invd) {
+    constexpr float rz = kSegThr + kSegMargin;
+    return fminf(fminf(seg_first_in(j0, v, invd, -0.5f, kSegMargin), seg_first_in(j0, v, invd, 0.0f, rz)),
+                 fminf(seg_first_in(j0, v, invd, 0.5f, kSegMargin), seg_first_in(j0, v, invd, 1.0f, rz)));
+}
+
+// Next slow channel (absolute) at or after run-relative j0; kSegNone if none before the run's end.
+__device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const AxisSeg& A, const AxisSeg& B,
+                                             const AxisSeg& C) {
+    const float jf = (float)j0;
+    const float f = fminf(fminf(seg_slow_axis(jf, A.v, A.invd), seg_slow_axis(jf, B.v, B.invd)),
+                          seg_slow_axis(jf, C.v, C.invd));
+    return f < (float)len ? b + (int)f : kSegNone;
+}
+
+template <int IDX>
+__device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const double2* __restrict__ sch,
+                                                     const RunF64* __restrict__ sru, double Sa, double Sb,
+                                                     double Sc) {
+    const double* __restrict__ tab = static_cast<const double*>(P.table);
+    const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
+    double acc = 0.0;
+    for (int ri = 0; ri < P.n_runs; ++ri) {
+        const RunF64 run = sru[ri];
+        const int b = run.begin, e = run.end, len = e - b;
+        const double ivb = sch[b].x;
+        AxisSeg A = axis_seg(Sa, ivb, run.delta, P.n_cells_d[0], len);
+        AxisSeg B = axis_seg(Sb, ivb, run.delta, P.n_cells_d[1], len);
+        AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
+        // segments: F^2 of the current one, and of the one after the next crossing (prefetched)
+        double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
+        int cross = min(min(A.c, B.c), C.c);  // run-relative
+        double F2n = 0.0;
+        if (cross != kSegNone)
+            F2n = f2_f64<IDX>(P, tab, l0, A.n + (cross >= A.c ? A.dn : 0), B.n + (cross >= B.c ? B.dn : 0),
+                              C.n + (cross >= C.c ? C.dn : 0));
+        int next_cross = cross == kSegNone ? kSegNone : b + cross;
+        int next_slow = seg_next_slow(0, b, len, A, B, C);
+        int next_ev = min(next_cross, next_slow);
+        double seg = 0.0;
+#pragma unroll kRecUnroll
+        for (int k = b; k < e; ++k) {
+            bool skip = false;
+            if (k == next_ev) {  // rare per lane
+                if (k == next_cross) {  // an axis index changes: flush, switch to the prefetched F^2
+                    acc = __fma_rn(F2, seg, acc);
+                    seg = 0.0;
+                    F2 = F2n;
+                    const int j = k - b;
+                    const int ca = A.c > j ? A.c : kSegNone, cb = B.c > j ? B.c : kSegNone,
+                              cc = C.c > j ? C.c : kSegNone;
+                    const int nx = min(min(ca, cb), cc);
+                    next_cross = nx == kSegNone ? kSegNone : b + nx;
+                    if (nx != kSegNone)
+                        F2n = f2_f64<IDX>(P, tab, l0, A.n + (nx >= A.c ? A.dn : 0), B.n + (nx >= B.c ? B.dn : 0),
+                                          C.n + (nx >= C.c ? C.dn : 0));
+                }
+                if (k == next_slow) {  // the exact reduced-phase form, exact index
+                    asm volatile("");
+                    const double2 c = sch[k];
+                    const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
+                    const AxisF64 bb = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
+                    const AxisF64 cc = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
+                    const double F2x = f2_f64<IDX>(P, tab, l0, __double2int_rn(a.n), __double2int_rn(bb.n),
+                                                   __double2int_rn(cc.n));
+                    const double ratio = ((a.num * bb.num) * cc.num) / ((a.den * bb.den) * cc.den);
+                    acc = __fma_rn(F2x * c.y, ratio * ratio, acc);  // 0/0 at t == 0: limit re-run
+                    skip = true;
+                    next_slow = seg_next_slow(k + 1 - b, b, len, A, B, C);
+                }
+                next_ev = min(next_cross, next_slow);
+            }
+            const double wt = sch[k].y;
+            const double nn = (A.num.s * B.num.s) * C.num.s;
+            const double dd = (A.den.s * B.den.s) * C.den.s;
+            const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+            if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
+            advance(A.den);
+            advance(A.num);
+            advance(B.den);
+            advance(B.num);
+            advance(C.den);
+            advance(C.num);
+        }
+        acc = __fma_rn(F2, seg, acc);
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
 // The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path, 2 = FP64 path with
-// the channel recurrence (sincg only).
+// the channel recurrence (sincg only), 3 = the segmented recurrence.
 // ---------------------------------------------------------------------------
 template <int COMPUTE, int SHAPE, int IDX, int PDEG>
 __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMPUTE>) spots_kernel(const SpotsParams P) {
@@ -576,6 +767,10 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
         double2* s = reinterpret_cast<double2*>(smem_raw);
         const double2* g = static_cast<const double2*>(P.chan);
         for (int i = tid; i < P.n_src; i += kBlockX * kBY) s[i] = g[i];
+        if constexpr (COMPUTE == 3) {
+            RunF64* r = reinterpret_cast<RunF64*>(smem_raw + 16 * P.n_src);
+            for (int i = tid; i < P.n_runs; i += kBlockX * kBY) r[i] = P.runs[i];
+        }
         if constexpr (COMPUTE == 2) {
             RunF64* r = reinterpret_cast<RunF64*>(smem_raw + 16 * P.n_src);
             for (int i = tid; i < P.n_runs; i += kBlockX * kBY) r[i] = P.runs[i];
@@ -644,6 +839,12 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
                             P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src),
                             reinterpret_cast<const float*>(smem_raw + 16 * P.n_src + sizeof(RunF64) * P.n_runs),
                             Sa, Sb, Sc);
+                        if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
+                        sub += a;
+                    } else if constexpr (COMPUTE == 3) {
+                        const double2* sch = reinterpret_cast<const double2*>(smem_raw);
+                        double a = domain_sum_f64_seg<IDX>(
+                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), Sa, Sb, Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;
                     } else {
@@ -864,6 +1065,11 @@ static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape
         const size_t smem = (size_t)P.n_src * 16;
         return idx == kIdxHash ? launch_shape<0, kIdxHash>(P, shape, smem, st)
                                : launch_shape<0, kIdxWide>(P, shape, smem, st);
+    }
+    if (compute == 6) {  // FP64 segmented channel recurrence (sincg)
+        const size_t smem = (size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64);
+        return idx == kIdxHash ? launch_t<3, 0, kIdxHash, kPolyF32>(P, smem, st)
+                               : launch_t<3, 0, kIdxWide, kPolyF32>(P, smem, st);
     }
     if (compute == 4) {  // FP64 channel recurrence (sincg)
         const size_t smem = (size_t)P.n_src * 20 + (size_t)P.n_runs * sizeof(RunF64);  // + FP32 1/lambda

@@ -698,7 +698,9 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                         double dev = 0.0;
                         for (int k = 0; k < len; ++k)
                             dev = std::max(dev, std::fabs(iv[order[b + k]] - iv[order[b]] - (double)k * delta));
-                        if (len == 1 || dev * smax <= 1e-14) {
+                        // segmented variant: at most one index change per axis per run
+                        const bool span_ok = len == 1 || smax * std::fabs(delta) * (double)(len - 1) <= 0.9;
+                        if (len == 1 || (dev * smax <= 1e-14 && span_ok)) {
                             runs.push_back(nbx::RunF64{iv[order[b]], delta, b, e});
                             break;
                         }
@@ -719,7 +721,8 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             plan->chan.ensure(ch.size() * sizeof(double));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice));
             if (!runs.empty()) {
-                plan->kernel_variant = 4;
+                // 6: segmented recurrence (default); NBX_FP64_REC=1: the per-channel bracket variant
+                plan->kernel_variant = (rev && std::atoi(rev) == 1) ? 4 : 6;
                 plan->runs.ensure(runs.size() * sizeof(nbx::RunF64));
                 NBX_CUDA(cudaMemcpy(plan->runs.p, runs.data(), runs.size() * sizeof(nbx::RunF64),
                                     cudaMemcpyHostToDevice));

@@ -9,6 +9,9 @@ keep working.
 """
 from __future__ import annotations
 
+import sys
+from types import ModuleType
+
 __all__ = [
     "XtraceError",
     "InvalidCellError",
@@ -18,6 +21,7 @@ __all__ = [
     "NumericalFault",
     "PatternFault",
     "NativeError",
+    "hierarchy_for",
 ]
 
 
@@ -64,3 +68,23 @@ class NativeError(XtraceError, RuntimeError):
 
     There is deliberately no CPU fallback: the product path fails loudly.
     """
+
+
+def hierarchy_for(*objs) -> ModuleType:
+    """The module whose error classes a call on ``objs`` raises.
+
+    When the inputs are the reference's own objects (``xtrace.kernels.SpotsContext``,
+    ``xtrace.kernels.PixelBuffer``, ...) the drop-in raises the reference's classes
+    (``xtrace.errors.ShapeMismatchError`` / ``PatternFault`` / ``NumericalFault``,
+    errors.py:20-39 of the reference), so ``except (NumericalFault, PatternFault)`` in the
+    reference's own callers (scheduler.py:212) catches them; otherwise this module's.
+    """
+    for o in objs:
+        top = type(o).__module__.partition(".")[0]
+        if not top or top == __name__.partition(".")[0]:
+            continue
+        mod = sys.modules.get(top + ".errors")
+        if mod is not None and all(hasattr(mod, n) for n in ("ShapeMismatchError", "NumericalFault",
+                                                              "PatternFault")):
+            return mod
+    return sys.modules[__name__]

@@ -8,8 +8,11 @@ Same arguments, same in-place write into ``out.data``, same errors
 (ShapeMismatchError for dims/precision, PatternFault(label, pixel,
 NumericalFault(pixel)) for the lowest non-finite pixel).  The pixels are
 computed by the hand-written sm_100a kernel in csrc/ through the C ABI
-(include/nbx.h); ``executor`` is accepted for signature compatibility and
-only receives a timing record.  There is no CPU fallback.
+(include/nbx.h); ``executor`` is accepted for signature compatibility (the
+call logs no timing record of its own, as the reference's body does not:
+``kernel_timer`` around it does).  With the reference's own objects as inputs
+the errors raised are the reference's classes (``xtrace.errors``).  There is
+no CPU fallback.
 
 Extensions (all default to the reference behaviour):
   SpotsContext.compute  "fp64" (default; the reference's FP64 arithmetic) or
@@ -28,6 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
+from . import errors as _errors
 from .errors import ShapeMismatchError
 from .model import BeamSpectrum, CrystalModel, Detector, DetectorPanel, PhiScan
 
@@ -187,14 +191,15 @@ def _dims_of(panel) -> tuple[int, int]:
     return panel.dims
 
 
-def _check_out(out: PixelBuffer, panel):
+def _check_out(out: PixelBuffer, panel, errors=None):
     # kernels.py:204-208 (f64 is accepted here as an extension)
+    err = (errors or _errors).ShapeMismatchError
     if out.dims != _dims_of(panel):
-        raise ShapeMismatchError(f"buffer dims {out.dims} != panel dims {_dims_of(panel)}")
+        raise err(f"buffer dims {out.dims} != panel dims {_dims_of(panel)}")
     if out.precision not in _DTYPES:
-        raise ShapeMismatchError(f"unsupported buffer precision {out.precision}")
+        raise err(f"unsupported buffer precision {out.precision}")
     if not (out.data.flags.c_contiguous and out.data.flags.writeable):
-        raise ShapeMismatchError("output buffer must be a contiguous writeable array")
+        raise err("output buffer must be a contiguous writeable array")
 
 
 def nanobragg_spots(ctx: SpotsContext, out: PixelBuffer, executor=None) -> None:
@@ -203,8 +208,8 @@ def nanobragg_spots(ctx: SpotsContext, out: PixelBuffer, executor=None) -> None:
     out[p] = r_e^2 * fluence / (sum(w) * n_domains * oversample^2)
              * sum_{sub, domain, source} w * Omega*pol(sub) * (F_cell * F_latt)^2
     """
-    _check_out(out, ctx.panel)
-    t0 = time.perf_counter()
+    errors = _errors.hierarchy_for(ctx, out)  # xtrace objects in -> xtrace.errors classes out
+    _check_out(out, ctx.panel, errors)
     desc = describe(ctx)
     cx = N.context()
     mode = N.OUT_F32 if out.precision == "f32" else N.OUT_F64
@@ -213,11 +218,9 @@ def nanobragg_spots(ctx: SpotsContext, out: PixelBuffer, executor=None) -> None:
     with cx.lock:
         status = cx.lib.nbx_spots(cx.handle, N.C.byref(desc.c), compute, mode,
                                   out.data.ctypes.data, 0, N.C.byref(bad))
-        N.check(cx, status, bad.value)
-    if executor is not None and hasattr(executor, "timing_log"):
-        from .execution import TimingRecord
-
-        executor.timing_log.append(TimingRecord("nanobragg_spots", (time.perf_counter() - t0) * 1e3))
+        N.check(cx, status, bad.value, errors=errors)
+    # no timing record here: like the reference body (parallel_for_blocks, execution.py:207-224),
+    # the call itself logs nothing; callers time it with kernel_timer (execution.py:350-356)
 
 
 class SpotsPlan:
@@ -303,8 +306,8 @@ def add_background(profile, panel, spectrum, thickness_factor: float, out: Pixel
     out[p] = r_e^2 fluence thickness_factor / sum(w) * sum_w w f_bg(sin(theta)/lambda_w)^2 * Omega*pol,
     at pixel centres.  f32 store (the reference) or f64 (extension).
     """
-    _check_out(out, panel)
-    t0 = time.perf_counter()
+    errors = _errors.hierarchy_for(profile, panel, spectrum, out)
+    _check_out(out, panel, errors)
     desc = _bg_descriptor(profile, panel, spectrum, thickness_factor)
     cx = N.context()
     bad = N.C.c_int64(-1)
@@ -312,11 +315,8 @@ def add_background(profile, panel, spectrum, thickness_factor: float, out: Pixel
     with cx.lock:
         status = cx.lib.nbx_background(cx.handle, N.C.byref(desc.c), mode, out.data.ctypes.data, 0,
                                        N.C.byref(bad))
-        N.check(cx, status, bad.value, label="add_background")
-    if executor is not None and hasattr(executor, "timing_log"):
-        from .execution import TimingRecord
-
-        executor.timing_log.append(TimingRecord("add_background", (time.perf_counter() - t0) * 1e3))
+        N.check(cx, status, bad.value, label="add_background", errors=errors)
+    # no timing record (the reference body logs nothing; kernel_timer does)
 
 
 def simulate_image(ctx, background=None, thickness_factor: float = 1.0, out: PixelBuffer | None = None,
