@@ -161,7 +161,7 @@ constexpr int kBlockY = NBX_BLOCK_Y;
 #define NBX_BLOCK_Y_SEG 4
 #endif
 #ifndef NBX_MIN_BLOCKS_SEG
-#define NBX_MIN_BLOCKS_SEG 5
+#define NBX_MIN_BLOCKS_SEG 6
 #endif
 template <int COMPUTE>
 constexpr int kBlockYOf = COMPUTE == 2 ? NBX_BLOCK_Y_REC : (COMPUTE == 3 ? NBX_BLOCK_Y_SEG : NBX_BLOCK_Y);
@@ -604,6 +604,10 @@ __device__ __forceinline__ double domain_sum_f64_rec(const SpotsParams& P, const
 constexpr float kSegThr = 3.2e-5f;      // |t| below this: the channel is evaluated directly
 constexpr float kSegMargin = 2e-6f;     // FP32 prediction margin (phase units)
 constexpr int kSegNone = 0x3FFFFFFF;
+#ifndef NBX_SEG_UNROLL
+#define NBX_SEG_UNROLL 4
+#endif
+constexpr int kSegUnroll = NBX_SEG_UNROLL;
 constexpr double kPi = 3.14159265358979323846;
 
 // sin(pi x)/pi for |x| <= 0.52 (degree-7 Q, rel err 2.9e-16)
@@ -665,21 +669,32 @@ __device__ __forceinline__ float seg_slow_axis(float j0, float v, float invd) {
                  fminf(seg_first_in(j0, v, invd, 0.5f, kSegMargin), seg_first_in(j0, v, invd, 1.0f, rz)));
 }
 
+// Per-thread event state, kept in shared memory (read only at events) so that the channel
+// loop's registers hold just the six sine sequences and the sums.
+struct SegThread {
+    double S[3];      // Sa, Sb, Sc (slow channels)
+    double f2[3];     // F^2 after the 1st, 2nd, 3rd index change of the run
+    int c[4];         // absolute channels of the index changes, ascending; kSegNone-terminated
+    float v[3], invd[3];
+};
+
 // Next slow channel (absolute) at or after run-relative j0; kSegNone if none before the run's end.
-__device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const AxisSeg& A, const AxisSeg& B,
-                                             const AxisSeg& C) {
+__device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const SegThread& T) {
     const float jf = (float)j0;
-    const float f = fminf(fminf(seg_slow_axis(jf, A.v, A.invd), seg_slow_axis(jf, B.v, B.invd)),
-                          seg_slow_axis(jf, C.v, C.invd));
+    const float f = fminf(fminf(seg_slow_axis(jf, T.v[0], T.invd[0]), seg_slow_axis(jf, T.v[1], T.invd[1])),
+                          seg_slow_axis(jf, T.v[2], T.invd[2]));
     return f < (float)len ? b + (int)f : kSegNone;
 }
 
 template <int IDX>
 __device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const double2* __restrict__ sch,
-                                                     const RunF64* __restrict__ sru, double Sa, double Sb,
-                                                     double Sc) {
+                                                     const RunF64* __restrict__ sru, SegThread& T, unsigned lanes,
+                                                     double Sa, double Sb, double Sc) {
     const double* __restrict__ tab = static_cast<const double*>(P.table);
     const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
+    T.S[0] = Sa;
+    T.S[1] = Sb;
+    T.S[2] = Sc;
     double acc = 0.0;
     for (int ri = 0; ri < P.n_runs; ++ri) {
         const RunF64 run = sru[ri];
@@ -688,60 +703,91 @@ __device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const
         AxisSeg A = axis_seg(Sa, ivb, run.delta, P.n_cells_d[0], len);
         AxisSeg B = axis_seg(Sb, ivb, run.delta, P.n_cells_d[1], len);
         AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
-        // segments: F^2 of the current one, and of the one after the next crossing (prefetched)
+        T.v[0] = A.v, T.v[1] = B.v, T.v[2] = C.v;
+        T.invd[0] = A.invd, T.invd[1] = B.invd, T.invd[2] = C.invd;
+        // the run's index changes in channel order (at most one per axis), F^2 after each
         double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
-        int cross = min(min(A.c, B.c), C.c);  // run-relative
-        double F2n = 0.0;
-        if (cross != kSegNone)
-            F2n = f2_f64<IDX>(P, tab, l0, A.n + (cross >= A.c ? A.dn : 0), B.n + (cross >= B.c ? B.dn : 0),
-                              C.n + (cross >= C.c ? C.dn : 0));
-        int next_cross = cross == kSegNone ? kSegNone : b + cross;
-        int next_slow = seg_next_slow(0, b, len, A, B, C);
+        {
+            int x = A.c, y = B.c, z = C.c;  // sort three
+            if (x > y) { const int q = x; x = y; y = q; }
+            if (y > z) { const int q = y; y = z; z = q; }
+            if (x > y) { const int q = x; x = y; y = q; }
+            const int cs[3] = {x, y, z};
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int ci = cs[i];
+                T.c[i] = ci == kSegNone ? kSegNone : b + ci;
+                if (ci != kSegNone)
+                    T.f2[i] = f2_f64<IDX>(P, tab, l0, A.n + (ci >= A.c ? A.dn : 0), B.n + (ci >= B.c ? B.dn : 0),
+                                          C.n + (ci >= C.c ? C.dn : 0));
+            }
+            T.c[3] = kSegNone;
+        }
+        int ev = 0;  // next index change
+        int next_cross = T.c[0];
+        int next_slow = seg_next_slow(0, b, len, T);
         int next_ev = min(next_cross, next_slow);
         double seg = 0.0;
-#pragma unroll kRecUnroll
-        for (int k = b; k < e; ++k) {
+        int k = b;
+        for (;;) {
+            // warp-uniform stop: the first channel at which some lane of the warp has an event
+            const int stop = min(__reduce_min_sync(lanes, next_ev), e);
+            // channels before it need no test at all
+#pragma unroll kSegUnroll
+            for (; k < stop; ++k) {
+                const double wt = sch[k].y;
+                const double nn = (A.num.s * B.num.s) * C.num.s;
+                const double dd = (A.den.s * B.den.s) * C.den.s;
+                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+                seg = __fma_rn(wt, ratio * ratio, seg);
+                advance(A.den);
+                advance(A.num);
+                advance(B.den);
+                advance(B.num);
+                advance(C.den);
+                advance(C.num);
+            }
+            if (k >= e) break;
             bool skip = false;
-            if (k == next_ev) {  // rare per lane
+            if (k == next_ev) {  // this lane's event (divergent, rare)
                 if (k == next_cross) {  // an axis index changes: flush, switch to the prefetched F^2
                     acc = __fma_rn(F2, seg, acc);
                     seg = 0.0;
-                    F2 = F2n;
-                    const int j = k - b;
-                    const int ca = A.c > j ? A.c : kSegNone, cb = B.c > j ? B.c : kSegNone,
-                              cc = C.c > j ? C.c : kSegNone;
-                    const int nx = min(min(ca, cb), cc);
-                    next_cross = nx == kSegNone ? kSegNone : b + nx;
-                    if (nx != kSegNone)
-                        F2n = f2_f64<IDX>(P, tab, l0, A.n + (nx >= A.c ? A.dn : 0), B.n + (nx >= B.c ? B.dn : 0),
-                                          C.n + (nx >= C.c ? C.dn : 0));
+                    do {  // every change at this channel (two axes may cross together)
+                        F2 = T.f2[ev];
+                        next_cross = T.c[++ev];
+                    } while (next_cross == k);
                 }
                 if (k == next_slow) {  // the exact reduced-phase form, exact index
                     asm volatile("");
                     const double2 c = sch[k];
-                    const AxisF64 a = axis_f64<kPolyF64, false>(Sa, c.x, P.n_cells_d[0]);
-                    const AxisF64 bb = axis_f64<kPolyF64, false>(Sb, c.x, P.n_cells_d[1]);
-                    const AxisF64 cc = axis_f64<kPolyF64, false>(Sc, c.x, P.n_cells_d[2]);
+                    const double S0 = T.S[0], S1 = T.S[1], S2 = T.S[2];
+                    const AxisF64 a = axis_f64<kPolyF64, false>(S0, c.x, P.n_cells_d[0]);
+                    const AxisF64 bb = axis_f64<kPolyF64, false>(S1, c.x, P.n_cells_d[1]);
+                    const AxisF64 cc = axis_f64<kPolyF64, false>(S2, c.x, P.n_cells_d[2]);
                     const double F2x = f2_f64<IDX>(P, tab, l0, __double2int_rn(a.n), __double2int_rn(bb.n),
                                                    __double2int_rn(cc.n));
                     const double ratio = ((a.num * bb.num) * cc.num) / ((a.den * bb.den) * cc.den);
                     acc = __fma_rn(F2x * c.y, ratio * ratio, acc);  // 0/0 at t == 0: limit re-run
                     skip = true;
-                    next_slow = seg_next_slow(k + 1 - b, b, len, A, B, C);
+                    next_slow = seg_next_slow(k + 1 - b, b, len, T);
                 }
                 next_ev = min(next_cross, next_slow);
             }
-            const double wt = sch[k].y;
-            const double nn = (A.num.s * B.num.s) * C.num.s;
-            const double dd = (A.den.s * B.den.s) * C.den.s;
-            const double ratio = nn * rcp_f64<kNewtonF64>(dd);
-            if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
-            advance(A.den);
-            advance(A.num);
-            advance(B.den);
-            advance(B.num);
-            advance(C.den);
-            advance(C.num);
+            {
+                const double wt = sch[k].y;
+                const double nn = (A.num.s * B.num.s) * C.num.s;
+                const double dd = (A.den.s * B.den.s) * C.den.s;
+                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+                if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
+                advance(A.den);
+                advance(A.num);
+                advance(B.den);
+                advance(B.num);
+                advance(C.den);
+                advance(C.num);
+            }
+            ++k;
         }
         acc = __fma_rn(F2, seg, acc);
     }
@@ -783,7 +829,10 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
     const DevPanel& pan = P.panels[blockIdx.z];
     const int f = blockIdx.x * kBlockX + threadIdx.x;
     const int sl = P.row0 + blockIdx.y * kBY + threadIdx.y;
-    if (sl >= pan.slow || sl >= P.max_slow || f >= pan.fast) return;
+    const bool inside = !(sl >= pan.slow || sl >= P.max_slow || f >= pan.fast);
+    // lanes of this warp that hold a pixel (the segmented loop's warp-uniform stops)
+    const unsigned lanes = COMPUTE == 3 ? __ballot_sync(0xFFFFFFFFu, inside) : 0u;
+    if (!inside) return;
 
     const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
     const double ps = pan.pixel_size;
@@ -843,8 +892,11 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
                         sub += a;
                     } else if constexpr (COMPUTE == 3) {
                         const double2* sch = reinterpret_cast<const double2*>(smem_raw);
+                        SegThread* st = reinterpret_cast<SegThread*>(
+                            smem_raw + ((16 * P.n_src + sizeof(RunF64) * P.n_runs + 15) & ~(size_t)15));
                         double a = domain_sum_f64_seg<IDX>(
-                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), Sa, Sb, Sc);
+                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), st[tid], lanes, Sa, Sb,
+                            Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;
                     } else {
@@ -1067,7 +1119,8 @@ static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape
                                : launch_shape<0, kIdxWide>(P, shape, smem, st);
     }
     if (compute == 6) {  // FP64 segmented channel recurrence (sincg)
-        const size_t smem = (size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64);
+        const size_t smem = (((size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64) + 15) & ~(size_t)15) +
+                            sizeof(SegThread) * kBlockX * kBlockYOf<3>;
         return idx == kIdxHash ? launch_t<3, 0, kIdxHash, kPolyF32>(P, smem, st)
                                : launch_t<3, 0, kIdxWide, kPolyF32>(P, smem, st);
     }

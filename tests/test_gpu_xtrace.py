@@ -101,7 +101,7 @@ def test_rank_task_flags_overflow_images_like_the_reference(xtrace, monkeypatch,
     """A float32-overflowing image is flagged (index, lowest bad pixel), not a rank error."""
     import paper_2205_07976_b200 as nbx
 
-    config = small_config(xtrace, fluence=1e24, default_f=1e20)  # spot peaks ~1e38+ overflow f32
+    config = small_config(xtrace, fluence=1e24, default_f=1e23)  # some pixels overflow f32 (first: 99)
     want = _rank(xtrace, config, 2)  # the unpatched reference (NumPy) on the same images
     assert want["error"] is None and len(want["flagged"]) == 2, want["flagged"]
     for mod in (xtrace.kernels, xtrace.scheduler):
@@ -123,7 +123,7 @@ def test_reference_error_classes(xtrace, gpu):
     from paper_2205_07976_b200 import errors as ours
 
     xk, xe = xtrace.kernels, xtrace.errors
-    config = small_config(xtrace, default_f=1e20)
+    config = small_config(xtrace, default_f=6e22)
     ctx = xk.SpotsContext(config.crystal_for_seed(3), config.panel, config.spectrum, 1)
     with pytest.raises(xe.PatternFault) as ref:  # the unpatched reference body (kernels.py:211-216)
         xk.nanobragg_spots(ctx, xk.PixelBuffer.zeros(config.panel.dims, "f32"))
