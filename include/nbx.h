@@ -32,12 +32,14 @@ extern "C" {
 
 /* Status codes.  NBX_ERR_ARG mirrors ShapeMismatchError / ValueError
  * (kernels.py:204-208), NBX_ERR_NUMERICAL mirrors NumericalFault wrapped in
- * PatternFault (kernels.py:211-216, execution.py:183-185). */
+ * PatternFault (kernels.py:211-216, execution.py:183-185), NBX_ERR_IO a file that could
+ * not be written (CampaignIOError, errors.py:55-61). */
 enum {
     NBX_OK = 0,
     NBX_ERR_ARG = 1,
     NBX_ERR_NUMERICAL = 2,
-    NBX_ERR_CUDA = 3
+    NBX_ERR_CUDA = 3,
+    NBX_ERR_IO = 4
 };
 
 /* Arithmetic path of the per-step evaluation. */
@@ -198,10 +200,19 @@ void nbx_plan_destroy(void* plan);
  * write_image io.py:403-434): image i of descs is rendered as NBX_OUT_IMAGE_F32 and its raw
  * little-endian float32 payload written to paths[i]; crcs[i] receives zlib.crc32 of the payload
  * (the caller writes the JSON sidecar).  The kernel of image i+1 runs while image i is copied
- * to the host, checksummed and written.  On a fault, *first_bad = (image << 40) | pixel and the
- * images after it are not written. */
+ * to the host, checksummed and written.  image_fault[i] (n_images entries) reports each image:
+ *   -1                  written (crcs[i] valid);
+ *   (0 << 40) | pixel   non-finite spot pixel, (1 << 40) | pixel non-finite background pixel:
+ *                       the image is FLAGGED and skipped and the campaign continues (the
+ *                       reference's _rank_task catches the fault and flags it, scheduler.py:212);
+ *   (2 << 40) | pixel   the f32 payload is non-finite (write_image refuses it, io.py:409-411; in
+ *                       the reference this aborts the rank): the campaign stops, NBX_ERR_NUMERICAL;
+ *   -3                  the file could not be written: the campaign stops, NBX_ERR_IO (the
+ *                       reference's CampaignIOError, scheduler.py:219-225);
+ *   -2                  not run (after a stop).
+ * Returns NBX_OK when every image was either written or flagged. */
 int nbx_campaign(void* ctx, const nbx_spots_desc* descs, int n_images, int compute,
-                 const char* const* paths, uint32_t* crcs, int64_t* first_bad);
+                 const char* const* paths, uint32_t* crcs, int64_t* image_fault);
 
 /* Image statistics over n values (dtype 0 f32, 1 f64): out = {min, max, mean, total}
  * (image_stats, kernels.py:346-371), the total bit for bit the reference's: NumPy's
@@ -244,6 +255,19 @@ int nbx_ipc_close(void* ctx, void* dev);
 /* out = mode(scale * sum_{r < n_slots} slots[r*n + p]), summed in rank order (deterministic). */
 int nbx_reduce_slots(void* ctx, const double* slots, int n_slots, int64_t n, double scale, int out_mode,
                      void* out, int out_on_device, int64_t* first_bad);
+
+/* One image split by energy channel over the ranks of a caller's NCCL communicator (SURVEY §8
+ * E1, config C5; the north star's "energy-channel shards summed with an NCCL reduce"): every
+ * rank calls it with the SAME descriptor (the whole spectrum); rank r evaluates its contiguous
+ * source shard (sizes within one, scheduler.py:138-153 plan_batches) into an unscaled FP64
+ * partial with the global normalisation (kernels.py:243-245), the partials are summed in place
+ * by ncclReduce(ncclFloat64, ncclSum) to `root` on the context's stream, and the root scales
+ * and stores the image (out_mode F32 / F64 / ADD_F64, as nbx_finalize; other ranks may pass
+ * out = NULL).  nccl_comm is an ncclComm_t; NCCL is resolved from the library already loaded
+ * in the process (the one that created the communicator), libnbx does not link it.  Returns
+ * after the reduce completed on this rank's stream. */
+int nbx_spots_reduce(void* ctx, const nbx_spots_desc* d, int compute, void* nccl_comm, int root,
+                     int out_mode, void* out, int out_on_device, int64_t* first_bad);
 
 /* lhs[j] += (double) rhs[j] -- add_array (kernels.py:315-331). */
 int nbx_add_array(void* ctx, double* lhs, const float* rhs, int64_t n, int on_device);

@@ -18,7 +18,7 @@ from .errors import NativeError
 
 LIB_PATH = Path(os.environ.get("NBX_LIB") or Path(__file__).resolve().parent / "_lib" / "libnbx.so")
 
-NBX_OK, NBX_ERR_ARG, NBX_ERR_NUMERICAL, NBX_ERR_CUDA = 0, 1, 2, 3
+NBX_OK, NBX_ERR_ARG, NBX_ERR_NUMERICAL, NBX_ERR_CUDA, NBX_ERR_IO = 0, 1, 2, 3, 4
 COMPUTE = {"fp64": 0, "fp32": 1}
 OUT_F32, OUT_F64, OUT_ADD_F64, OUT_RAW_F64, OUT_IMAGE_F64, OUT_IMAGE_F32, OUT_RAW_STORE_F64 = 0, 1, 2, 3, 4, 5, 6
 SHAPES = {"sincg": 0, "square": 0, "gauss": 1, "round": 2, "tophat": 3}
@@ -29,7 +29,7 @@ EXPORTS = (
     "nbx_ctx_synchronize", "nbx_output_pixels", "nbx_spots", "nbx_spots_batch", "nbx_plan_create",
     "nbx_plan_run", "nbx_plan_info", "nbx_plan_last_kernel_ms", "nbx_plan_destroy", "nbx_finalize",
     "nbx_add_array", "nbx_add_noise", "nbx_poisson_host", "nbx_probe_fma_peak", "nbx_background",
-    "nbx_fault_stage", "nbx_campaign", "nbx_crc32", "nbx_image_stats", "nbx_image_histogram",
+    "nbx_fault_stage", "nbx_spots_reduce", "nbx_campaign", "nbx_crc32", "nbx_image_stats", "nbx_image_histogram",
     "nbx_struct_size", "nbx_device_count", "nbx_ipc_alloc", "nbx_ipc_free", "nbx_ipc_open", "nbx_ipc_close", "nbx_reduce_slots",
 )
 
@@ -105,6 +105,8 @@ def load() -> C.CDLL:
             "nbx_probe_fma_peak": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
             "nbx_background": (C.c_int, [vp, C.POINTER(SpotsDesc), C.c_int, vp, C.c_int, i64p]),
             "nbx_fault_stage": (C.c_int, [vp]),
+            "nbx_spots_reduce": (C.c_int, [vp, C.POINTER(SpotsDesc), C.c_int, vp, C.c_int, C.c_int, vp, C.c_int,
+                                           i64p]),
             "nbx_campaign": (C.c_int, [vp, C.POINTER(SpotsDesc), C.c_int, C.c_int, C.POINTER(C.c_char_p),
                                        C.POINTER(C.c_uint32), i64p]),
             "nbx_crc32": (C.c_uint32, [C.c_uint32, vp, C.c_int64]),

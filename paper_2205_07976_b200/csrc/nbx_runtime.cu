@@ -7,10 +7,14 @@
 // entry point catches and converts to an NBX_* status + last-error string.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cerrno>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1357,12 +1361,16 @@ uint32_t nbx_crc32(uint32_t crc, const void* data, int64_t n) {
 }
 
 int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int compute, const char* const* paths,
-                 uint32_t* crcs, int64_t* first_bad) {
-    if (first_bad) *first_bad = -1;
-    int64_t bad_code = -1;
+                 uint32_t* crcs, int64_t* image_fault) {
+    constexpr int64_t kNotRun = -2, kIoFailed = -3;
+    int stop = NBX_OK;  // NBX_ERR_NUMERICAL (non-finite payload) or NBX_ERR_IO end the campaign early
+    std::string stop_msg;
+    if (image_fault)
+        for (int i = 0; i < n_images; ++i) image_fault[i] = kNotRun;
     int st = guarded(ctxp, [&]() -> int {
         if (!ctxp) throw ArgError("NULL context");
-        if (n_images < 0 || (n_images > 0 && (!descs || !paths || !crcs))) throw ArgError("invalid campaign arguments");
+        if (n_images < 0 || (n_images > 0 && (!descs || !paths || !crcs || !image_fault)))
+            throw ArgError("invalid campaign arguments");
         Ctx* ctx = static_cast<Ctx*>(ctxp);
         NBX_CUDA(cudaSetDevice(ctx->device));
         if (!ctx->copy_stream) NBX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
@@ -1417,13 +1425,35 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
             for (int q = 0; q < 2; ++q) NBX_CUDA(cudaMallocHost(&ctx->camp_host[q], max_bytes));
             ctx->camp_host_bytes = max_bytes;
         }
-        auto write_image = [&](int i, const void* data, size_t nbytes) {
+        // false (and the campaign stops) when the file cannot be written
+        auto write_image = [&](int i, const void* data, size_t nbytes) -> bool {
             crcs[i] = crc32_update(0, static_cast<const unsigned char*>(data), nbytes);
             FILE* fh = std::fopen(paths[i], "wb");
-            if (!fh) throw ArgError(std::string("cannot open ") + paths[i]);
-            const size_t wrote = std::fwrite(data, 1, nbytes, fh);
-            const int closed = std::fclose(fh);
-            if (wrote != nbytes || closed != 0) throw ArgError(std::string("short write to ") + paths[i]);
+            bool ok = fh != nullptr;
+            if (fh) {
+                ok = std::fwrite(data, 1, nbytes, fh) == nbytes;
+                ok = (std::fclose(fh) == 0) && ok;
+            }
+            if (!ok) {
+                image_fault[i] = kIoFailed;
+                stop = NBX_ERR_IO;
+                stop_msg = std::string("cannot write ") + paths[i] + ": " + std::strerror(errno);
+                return false;
+            }
+            image_fault[i] = -1;
+            return true;
+        };
+        // a fault of image i: spots / background stage -> flagged, the campaign continues;
+        // a non-finite f32 payload -> the campaign stops (write_image refuses it, io.py:409-411)
+        auto fault = [&](int i, int64_t pixel, int stage) -> bool {
+            image_fault[i] = ((int64_t)stage << 40) | pixel;
+            if (stage == 2) {
+                stop = NBX_ERR_NUMERICAL;
+                stop_msg = "refusing to write non-finite pixel " + std::to_string(pixel) + " of campaign image " +
+                           std::to_string(i);
+                return false;
+            }
+            return true;
         };
         bool any_long = false;  // a spectrum longer than one launch: nbx_spots' sharded image path
         for (int i = 0; i < n_images; ++i) {
@@ -1435,11 +1465,11 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                 int64_t bad = -1;
                 const int s2 = nbx_spots(ctx, descs + i, compute, NBX_OUT_IMAGE_F32, ctx->camp_host[0], 0, &bad);
                 if (s2 == NBX_ERR_NUMERICAL) {
-                    bad_code = ((int64_t)i << 40) | bad;
-                    return NBX_OK;
+                    if (!fault(i, bad, ctx->fault_stage)) return NBX_OK;
+                    continue;
                 }
                 if (s2 != NBX_OK) return s2;
-                write_image(i, ctx->camp_host[0], (size_t)count_pixels(descs + i) * 4);
+                if (!write_image(i, ctx->camp_host[0], (size_t)count_pixels(descs + i) * 4)) return NBX_OK;
             }
             return NBX_OK;
         }
@@ -1450,13 +1480,17 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
             NBX_CUDA(cudaEventSynchronize(copied[b]));
             const int64_t bad = pick_fault(ctx, hfault[b]);
             if (bad >= 0) {
-                bad_code = ((int64_t)i << 40) | bad;
+                if (fault(i, bad, ctx->fault_stage)) continue;  // flagged: skip the write, keep going
                 NBX_CUDA(cudaStreamSynchronize(cs));
                 NBX_CUDA(cudaStreamSynchronize(ds));
                 return NBX_OK;
             }
             const auto t0 = std::chrono::steady_clock::now();
-            write_image(i, ctx->camp_host[b], bytes[b]);
+            if (!write_image(i, ctx->camp_host[b], bytes[b])) {
+                NBX_CUDA(cudaStreamSynchronize(cs));
+                NBX_CUDA(cudaStreamSynchronize(ds));
+                return NBX_OK;
+            }
             if (trace_enabled()) {
                 const auto t1 = std::chrono::steady_clock::now();
                 std::fprintf(stderr, "[nbx] campaign image %d: crc + write %.2f ms\n", i,
@@ -1466,12 +1500,8 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
         return NBX_OK;
     });
     if (st != NBX_OK) return st;
-    if (bad_code >= 0) {
-        if (first_bad) *first_bad = bad_code;
-        set_err(ctxp, "non-finite value in campaign image " + std::to_string(bad_code >> 40));
-        return NBX_ERR_NUMERICAL;
-    }
-    return NBX_OK;
+    if (stop != NBX_OK) set_err(ctxp, stop_msg);
+    return stop;
 }
 
 int nbx_fault_stage(void* ctxp) { return ctxp ? static_cast<Ctx*>(ctxp)->fault_stage : 0; }
@@ -1662,6 +1692,93 @@ int nbx_reduce_slots(void* ctxp, const double* slots, int n_slots, int64_t n, do
     });
     if (st != NBX_OK) return st;
     return fault_status(ctxp, bad, first_bad);
+}
+
+// ---------------------------------------------------------------------------
+// Channel-sharded image over a caller's NCCL communicator (nbx_spots_reduce).  NCCL is
+// resolved at run time from the library already loaded in the process (the one that made
+// the communicator: torch's bundled copy, or the caller's), so libnbx has no link-time NCCL
+// dependency; ncclComm_t is an opaque pointer at this boundary.
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    int (*comm_count)(void*, int*) = nullptr;
+    int (*comm_user_rank)(void*, int*) = nullptr;
+    int (*reduce)(const void*, void*, size_t, int, int, int, void*, cudaStream_t) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+};
+
+const NcclApi* nccl_api() {
+    static std::once_flag once;
+    static NcclApi api;
+    std::call_once(once, [] {
+        void* h = nullptr;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_NOLOAD);  // the instance that created the communicator
+            if (h) break;
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.comm_count = reinterpret_cast<int (*)(void*, int*)>(dlsym(h, "ncclCommCount"));
+        api.comm_user_rank = reinterpret_cast<int (*)(void*, int*)>(dlsym(h, "ncclCommUserRank"));
+        api.reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, int, void*, cudaStream_t)>(
+            dlsym(h, "ncclReduce"));
+        api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    });
+    return api.comm_count && api.comm_user_rank && api.reduce ? &api : nullptr;
+}
+
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;  // ncclFloat64 / ncclSum (nccl.h)
+
+int nbx_spots_reduce(void* ctxp, const nbx_spots_desc* d, int compute, void* nccl_comm, int root, int out_mode,
+                     void* out, int out_on_device, int64_t* first_bad) {
+    if (first_bad) *first_bad = -1;
+    int rank = 0, world = 1;
+    int64_t npix = 0;
+    double scale = 0.0;
+    int st = guarded(ctxp, [&]() -> int {
+        if (!ctxp || !d) throw ArgError("NULL context or descriptor");
+        if (!nccl_comm) throw ArgError("NULL NCCL communicator");
+        const NcclApi* nc = nccl_api();
+        if (!nc) throw ArgError("NCCL is not loaded in this process (libnccl.so.2 not found)");
+        if (nc->comm_count(nccl_comm, &world) != 0 || nc->comm_user_rank(nccl_comm, &rank) != 0)
+            throw ArgError("invalid NCCL communicator");
+        if (root < 0 || root >= world) throw ArgError("root is not a rank of the communicator");
+        if (rank == root) {
+            if (out_mode != NBX_OUT_F32 && out_mode != NBX_OUT_F64 && out_mode != NBX_OUT_ADD_F64)
+                throw ArgError("reduce output mode must be F32, F64 or ADD_F64");
+            if (!out) throw ArgError("output buffer is NULL");
+        }
+        validate(d);
+        const int sb = d->src_begin, se = d->src_end <= 0 ? d->n_sources : d->src_end;
+        if (se - sb < world) throw ArgError("fewer sources than ranks");
+        Ctx* ctx = static_cast<Ctx*>(ctxp);
+        NBX_CUDA(cudaSetDevice(ctx->device));
+        npix = count_pixels(d);
+        // this rank's channel shard: contiguous, sizes within one, the first (n % world) one larger
+        // (plan_batches, scheduler.py:138-153); the GLOBAL normalisation (kernels.py:243-245)
+        nbx_spots_desc sh = *d;
+        const int n = se - sb, base = n / world, extra = n % world;
+        sh.src_begin = sb + rank * base + std::min(rank, extra);
+        sh.src_end = sh.src_begin + base + (rank < extra ? 1 : 0);
+        if (!(sh.norm > 0)) {
+            double wsum = 0.0;
+            for (int i = 0; i < d->n_sources; ++i) wsum += d->weights[i];
+            sh.norm = wsum * (double)d->n_domains * (double)(d->oversample * d->oversample);
+        }
+        scale = d->r_e_sqr * d->fluence / sh.norm;
+        ctx->raw_scratch.ensure((size_t)npix * sizeof(double));
+        double* raw = static_cast<double*>(ctx->raw_scratch.p);
+        const int s1 = nbx_spots(ctxp, &sh, compute, NBX_OUT_RAW_STORE_F64, raw, 1, nullptr);
+        if (s1 != NBX_OK) return s1;
+        const int r = nc->reduce(raw, raw, (size_t)npix, kNcclFloat64, kNcclSum, root, nccl_comm, ctx->stream);
+        if (r != 0)
+            throw CudaError(std::string("ncclReduce failed: ") + (nc->error_string ? nc->error_string(r) : "?"));
+        NBX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return NBX_OK;
+    });
+    if (st != NBX_OK || rank != root) return st;
+    return nbx_finalize(ctxp, static_cast<const double*>(static_cast<Ctx*>(ctxp)->raw_scratch.p), npix, scale,
+                        out_mode, out, out_on_device, first_bad);
 }
 
 int nbx_add_array(void* ctxp, double* lhs, const float* rhs, int64_t n, int on_device) {

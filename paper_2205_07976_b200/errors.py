@@ -21,6 +21,7 @@ __all__ = [
     "NumericalFault",
     "PatternFault",
     "NativeError",
+    "CampaignIOError",
     "hierarchy_for",
 ]
 
@@ -61,6 +62,15 @@ class PatternFault(XtraceError, RuntimeError):
         self.index = int(index)
         self.cause = cause
         super().__init__(f"pattern {label!r} failed at index {self.index}: {cause!r}")
+
+
+class CampaignIOError(XtraceError, OSError):
+    """Writing a campaign image failed (errors.py:55-61 of the reference); carries the image index."""
+
+    def __init__(self, image_index: int, cause):
+        self.image_index = int(image_index)
+        self.cause = cause
+        super().__init__(f"I/O failure on image {self.image_index}: {cause}")
 
 
 class NativeError(XtraceError, RuntimeError):

@@ -28,10 +28,10 @@ from typing import Callable, NamedTuple
 import numpy as np
 
 from . import _native as N
-from .errors import NumericalFault, PatternFault, ShapeMismatchError
+from .errors import CampaignIOError, NumericalFault, ShapeMismatchError
 from .kernels import PixelBuffer, describe
 
-__all__ = ["write_image", "read_image", "run_campaign", "CampaignResult", "image_stats", "image_histogram",
+__all__ = ["write_image", "read_image", "run_campaign", "campaign_indices", "CampaignResult", "image_stats", "image_histogram",
            "ImageStats", "HistogramResult", "image_stem"]
 
 _DOWNCAST = "values rounded to nearest-even from the float64 accumulator"
@@ -101,22 +101,27 @@ def read_image(path, verify_crc: bool = True) -> tuple[np.ndarray, dict]:
 
 @dataclass
 class CampaignResult:
+    """Images written (index, .bin path, payload CRC-32, in index order) and images flagged.
+
+    ``flagged`` holds (index, lowest non-finite pixel) for every image whose spots or
+    background faulted: like the reference's rank loop (scheduler.py:208-214) the image is
+    skipped and the campaign carries on.
+    """
     indices: list[int]
     paths: list[Path]
     crcs: list[int]
     seconds: float
+    flagged: list[tuple[int, int]] = None
+
+    def __post_init__(self):
+        if self.flagged is None:
+            self.flagged = []
 
 
-def run_campaign(context_for: Callable[[int], object], n_images: int, out_dir, *, first_image: int = 0,
-                 background=None, thickness_factor: float = 1.0, seeds: Callable[[int], int] | None = None,
-                 group=None, device: int | None = None) -> CampaignResult:
-    """Render images [first_image, first_image + n_images) (this rank's share) and write them.
-
-    ``context_for(index)`` returns the SpotsContext of image ``index`` (e.g. a
-    per-image seed, like SimulationConfig.crystal_for_seed, io.py:146-157).
-    """
-    import time
-
+def campaign_indices(n_images: int, first_image: int = 0, group=None) -> list[int]:
+    """This rank's images of [first_image, first_image + n_images): its contiguous block of the
+    reference's static partition (plan_batches, scheduler.py:138-153) over the ranks of
+    ``group`` when torch.distributed is initialised, else all of them."""
     world, rank = 1, 0
     try:
         import torch.distributed as dist
@@ -128,7 +133,24 @@ def run_campaign(context_for: Callable[[int], object], n_images: int, out_dir, *
     from .parallel import plan_batches
 
     _, (lo, hi) = plan_batches(n_images, world)[rank]
-    indices = list(range(first_image + lo, first_image + hi))
+    return list(range(first_image + lo, first_image + hi))
+
+
+def run_campaign(context_for: Callable[[int], object], n_images: int, out_dir, *, first_image: int = 0,
+                 background=None, thickness_factor: float = 1.0, seeds: Callable[[int], int] | None = None,
+                 group=None, device: int | None = None) -> CampaignResult:
+    """Render images [first_image, first_image + n_images) (this rank's share) and write them.
+
+    ``context_for(index)`` returns the SpotsContext of image ``index`` (e.g. a
+    per-image seed, like SimulationConfig.crystal_for_seed, io.py:146-157).  Like the
+    reference's rank loop (scheduler.py:190-247): an image whose spots or background are
+    non-finite is flagged in ``CampaignResult.flagged`` and skipped, the others are written;
+    a file that cannot be written raises CampaignIOError after the sidecars of every image
+    written before it; a non-finite float32 payload raises NumericalFault (write_image).
+    """
+    import time
+
+    indices = campaign_indices(n_images, first_image, group)
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
     ctxs = [context_for(i) for i in indices]
@@ -140,29 +162,35 @@ def run_campaign(context_for: Callable[[int], object], n_images: int, out_dir, *
     arr = (N.SpotsDesc * max(n, 1))(*[d.c for d in descs])
     cpaths = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
     crcs = (C.c_uint32 * max(n, 1))()
-    bad = C.c_int64(-1)
+    faults = (C.c_int64 * max(n, 1))()
     compute = N.COMPUTE[getattr(ctxs[0], "compute", "fp64")] if ctxs else 0
     t0 = time.perf_counter()
     with cx.lock:
-        status = cx.lib.nbx_campaign(cx.handle, arr, n, compute, cpaths, crcs, C.byref(bad))
-        stage = cx.lib.nbx_fault_stage(cx.handle)
-        msg = cx.error() if status not in (N.NBX_OK, N.NBX_ERR_NUMERICAL) else ""
+        status = cx.lib.nbx_campaign(cx.handle, arr, n, compute, cpaths, crcs, faults)
+        msg = cx.error() if status != N.NBX_OK else ""
     seconds = time.perf_counter() - t0
-    if status == N.NBX_ERR_NUMERICAL:
-        img, pix = bad.value >> 40, bad.value & ((1 << 40) - 1)
-        cause = NumericalFault(pix)
-        if stage == 2:  # write_image refuses the non-finite downcast (io.py:409-411)
-            raise NumericalFault(pix, f"image {indices[img]}: refusing to write non-finite pixel {pix}")
-        label = "nanobragg_spots" if stage == 0 else "add_background"
-        raise PatternFault(label, pix, cause) from cause
-    if status != N.NBX_OK:
+    if status not in (N.NBX_OK, N.NBX_ERR_NUMERICAL, N.NBX_ERR_IO):
         if status == N.NBX_ERR_ARG:
             raise ShapeMismatchError(msg) if "dims" in msg or "buffer" in msg else ValueError(msg)
         raise N.NativeError(msg)
-    for i, (stem, c, crc) in enumerate(zip(stems, ctxs, crcs)):
-        _write_sidecar(stem, _sidecar(c.panel.dims, crc, c.panel, c.spectrum,
-                                      seeds(indices[i]) if seeds else None, indices[i]))
-    return CampaignResult(indices, paths, [int(x) for x in crcs[:n]], seconds)
+    done, flagged = [], []
+    for i in range(n):
+        f = int(faults[i])
+        if f == -1:  # written: its sidecar (write_image writes .bin then .json, io.py:425-433)
+            _write_sidecar(stems[i], _sidecar(ctxs[i].panel.dims, crcs[i], ctxs[i].panel, ctxs[i].spectrum,
+                                              seeds(indices[i]) if seeds else None, indices[i]))
+            done.append(i)
+        elif f >= 0 and (f >> 40) in (0, 1):
+            flagged.append((indices[i], f & ((1 << 40) - 1)))
+    if status == N.NBX_ERR_NUMERICAL:  # a non-finite float32 payload: write_image refuses it (io.py:409-411)
+        i = next(j for j in range(n) if int(faults[j]) >= 0 and (int(faults[j]) >> 40) == 2)
+        pix = int(faults[i]) & ((1 << 40) - 1)
+        raise NumericalFault(pix, f"image {indices[i]}: refusing to write non-finite pixel {pix}")
+    if status == N.NBX_ERR_IO:  # the reference aborts the campaign (scheduler.py:219-225)
+        i = next(j for j in range(n) if int(faults[j]) == -3)
+        raise CampaignIOError(indices[i], msg)
+    return CampaignResult([indices[i] for i in done], [paths[i] for i in done], [int(crcs[i]) for i in done],
+                          seconds, flagged)
 
 
 class ImageStats(NamedTuple):

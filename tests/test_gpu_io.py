@@ -36,6 +36,49 @@ def test_campaign_files_equal_simulate_image_downcast(gpu, tmp_path, compute):
         assert np.array_equal(data.reshape(-1), acc.data.astype(np.float32))
 
 
+def hot_ctx_for(i, bad=(12,)):
+    """Image ``i`` of a campaign whose images in ``bad`` overflow float32 (fluence x 1e40)."""
+    import dataclasses
+
+    c = ctx_for(i, "fp64")
+    if i in bad:
+        c = dataclasses.replace(c, spectrum=dataclasses.replace(c.spectrum, fluence=c.spectrum.fluence * 1e40))
+    return c
+
+
+def test_campaign_flags_faulting_images_and_continues(gpu, tmp_path):
+    """A non-finite image is flagged (index, lowest bad pixel) and skipped; the images before and
+    after it are written with their sidecars -- the reference's rank loop (scheduler.py:208-214)."""
+    from paper_2205_07976_b200 import PatternFault, nanobragg_spots
+
+    res = nio.run_campaign(hot_ctx_for, 5, tmp_path, first_image=10, seeds=lambda i: synthetic.SEED + i)
+    assert res.indices == [10, 11, 13, 14]
+    with pytest.raises(PatternFault) as info:  # the pixel the drop-in reports for the same image
+        nanobragg_spots(hot_ctx_for(12), PixelBuffer.zeros((96, 128), "f32"))
+    assert res.flagged == [(12, info.value.index)]
+    assert not (tmp_path / "img_000012.bin").exists() and not (tmp_path / "img_000012.json").exists()
+    for idx, path in zip(res.indices, res.paths):
+        data, side = nio.read_image(path)
+        assert side["image_index"] == idx
+        acc = simulate_image(ctx_for(idx, "fp64"))
+        assert np.array_equal(data.reshape(-1), acc.data.astype(np.float32))
+
+
+def test_campaign_io_failure_aborts_after_writing_sidecars(gpu, tmp_path):
+    """An unwritable image file raises CampaignIOError(index) (scheduler.py:219-225); every image
+    written before it has its sidecar and reads back; the images after it are not rendered."""
+    from paper_2205_07976_b200.errors import CampaignIOError
+
+    (tmp_path / "img_000013.bin").mkdir()  # fopen(..., "wb") fails on a directory
+    with pytest.raises(CampaignIOError) as info:
+        nio.run_campaign(lambda i: ctx_for(i, "fp64"), 5, tmp_path, first_image=10)
+    assert info.value.image_index == 13 and isinstance(info.value, OSError)
+    for idx in (10, 11, 12):
+        data, side = nio.read_image(tmp_path / f"img_{idx:06d}.bin")
+        assert side["image_index"] == idx
+    assert not (tmp_path / "img_000014.bin").exists()
+
+
 def test_write_image_matches_reference_format(gpu, tmp_path):
     acc = simulate_image(ctx_for(0))
     p = nio.write_image(acc, tmp_path / "x", panel=ctx_for(0).panel, spectrum=ctx_for(0).spectrum, seed=3,

@@ -121,3 +121,119 @@ def test_p2p_channel_sharded_transport_two_ranks(gpu, tmp_path):
     d = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
     assert d["fp64"]["p2p_vs_reduce"] < 1e-15 and d["fp64"]["p2p_vs_whole"] < 1e-12, d
     assert d["fp32"]["p2p_vs_reduce"] < 1e-15 and d["fp32"]["p2p_vs_whole"] < 1e-4, d
+
+
+P2P_FAIL_SCRIPT = r'''
+import os, sys, json
+sys.path.insert(0, os.environ["NBX_ROOT"])
+import numpy as np
+import torch, torch.distributed as dist
+from paper_2205_07976_b200 import PixelBuffer, nanobragg_spots, parallel, synthetic
+from paper_2205_07976_b200 import kernels as K
+dist.init_process_group("gloo")
+torch.cuda.set_device(0)
+rank = dist.get_rank()
+panel = synthetic.roi(synthetic.rayonix_panel(), 1880, 1880, 24, 32)
+ctx = synthetic.ls49_context(panel=panel, n_channels=6, n_domains=2, compute="fp64")
+out = {}
+orig_run = K.SpotsPlan.run
+for phase, failing in (("kernel", 1), ("kernel", 0), ("setup", 1)):
+    def boom(self, *a, **k):
+        raise RuntimeError("injected kernel failure")
+    orig_init = K.SpotsPlan.__init__
+    def bad_init(self, *a, **k):
+        raise RuntimeError("injected set-up failure")
+    if rank == failing:
+        if phase == "kernel":
+            K.SpotsPlan.run = boom
+        else:
+            K.SpotsPlan.__init__ = bad_init
+    try:
+        parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(panel.dims, "f64"), transport="p2p")
+        out[f"{phase}{failing}"] = "no error"
+    except RuntimeError as e:
+        out[f"{phase}{failing}"] = str(e)
+    K.SpotsPlan.run = orig_run
+    K.SpotsPlan.__init__ = orig_init
+# after the failures the transport still works (slots freed, nothing left mapped)
+a = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(panel.dims, "f64"), transport="p2p")
+if rank == 0:
+    whole = PixelBuffer.zeros(panel.dims, "f64")
+    nanobragg_spots(ctx, whole)
+    out["after"] = float(np.abs(a.data - whole.data).max() / np.abs(whole.data).max())
+print(json.dumps({"rank": rank, **out}), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_p2p_channel_sharded_failure_on_one_rank(gpu, tmp_path):
+    """ADVICE r01: a rank failing in set-up or in its kernel makes EVERY rank raise (the failing
+    one its own error, the others 'failed on another rank') instead of hanging in a barrier or
+    freeing slots a peer still writes; the transport works again afterwards."""
+    script = tmp_path / "p2p_fail.py"
+    script.write_text(P2P_FAIL_SCRIPT)
+    env = dict(os.environ, NBX_ROOT=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29537", str(script)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rows = {r["rank"]: r for r in (json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{"))}
+    for key, failing in (("kernel1", 1), ("kernel0", 0), ("setup1", 1)):
+        for rank in (0, 1):
+            msg = rows[rank][key]
+            if rank == failing:
+                assert msg.startswith("injected"), (key, rank, msg)
+            else:
+                assert "another rank" in msg, (key, rank, msg)
+    assert rows[0]["after"] < 1e-12
+
+
+NATIVE_SCRIPT = r'''
+import ctypes as C, os, sys, json
+sys.path.insert(0, os.environ["NBX_ROOT"])
+import numpy as np
+import torch, torch.distributed as dist
+from paper_2205_07976_b200 import PixelBuffer, describe, nanobragg_spots, parallel, synthetic
+from paper_2205_07976_b200 import _native as N
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+panel = synthetic.roi(synthetic.rayonix_panel(), 1880, 1880, 40, 48)
+res = {}
+for compute in ("fp64", "fp32"):
+    ctx = synthetic.ls49_context(panel=panel, n_channels=9, n_domains=3, compute=compute)
+    got = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(panel.dims, "f32"), transport="native")
+    whole = PixelBuffer.zeros(panel.dims, "f32")
+    nanobragg_spots(ctx, whole)
+    res[compute] = {"bitwise": bool(np.array_equal(got.data, whole.data)),
+                    "rel": float(np.abs(got.data.astype(float) - whole.data).max() / whole.data.max())}
+# the C ABI's argument checks
+cx = N.context(0)
+desc = describe(synthetic.ls49_context(panel=panel, n_channels=9, n_domains=3, compute="fp64"))
+bad = C.c_int64(-1)
+out = np.zeros(panel.n_pixels, np.float32)
+comm = dist.distributed_c10d._get_default_group()._get_backend(torch.device("cuda"))._comm_ptr()
+res["null_comm"] = cx.lib.nbx_spots_reduce(cx.handle, C.byref(desc.c), 0, None, 0, N.OUT_F32, out.ctypes.data, 0,
+                                           C.byref(bad))
+res["bad_root"] = cx.lib.nbx_spots_reduce(cx.handle, C.byref(desc.c), 0, C.c_void_p(comm), 1, N.OUT_F32,
+                                          out.ctypes.data, 0, C.byref(bad))
+print(json.dumps(res), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_native_nccl_reduce_single_rank(gpu, tmp_path):
+    """nbx_spots_reduce (the C ABI's channel-sharded image over a caller's ncclComm_t) with torch's
+    one-rank NCCL communicator: the image equals nanobragg_spots bit for bit on both paths (one
+    shard = the whole spectrum, the same global scale); a NULL communicator or a root outside the
+    communicator is an argument error.  (NCCL refuses two ranks on one GPU: the multi-rank
+    arithmetic -- shards, global norm, reduce, root-side scale -- is the gloo world-8 suite's.)"""
+    script = tmp_path / "native.py"
+    script.write_text(NATIVE_SCRIPT)
+    env = dict(os.environ, NBX_ROOT=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", "29538", str(script)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-3000:]
+    d = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["fp64"]["bitwise"] and d["fp32"]["rel"] < 1e-6, d
+    assert d["null_comm"] == 1 and d["bad_root"] == 1, d
