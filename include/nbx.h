@@ -103,7 +103,8 @@ typedef struct nbx_spots_desc {
     const double* wavelengths;   /* n_sources, Angstrom, > 0 */
     const double* weights;       /* n_sources, >= 0 */
     double fluence;              /* photons / m^2 */
-    double r_e_sqr;              /* m^2 */
+    double r_e_sqr;              /* m^2, the spot stage; the background stage always uses the
+                                    reference module constant R_E_SQR (kernels.py:44,299) */
     /* crystal */
     int32_t n_domains;           /* mosaic domains x phi steps */
     int32_t shape;               /* NBX_SHAPE_* */
@@ -232,7 +233,8 @@ uint32_t nbx_crc32(uint32_t crc, const void* data, int64_t n);
  * thickness_factor, out) (kernels.py:279-312): pixel centres, one interpolated
  * f_bg(sin(theta)/lambda)^2 per source.  out_mode NBX_OUT_F32 (the reference's
  * store) / NBX_OUT_F64 / NBX_OUT_ADD_F64 (+= f64(f32), add_array fused).
- * Only panels, beam, spectrum, fluence, r_e_sqr and the bg_* fields are read. */
+ * Only panels, beam, spectrum, fluence and the bg_* fields are read (the scale uses the
+ * reference constant R_E_SQR, kernels.py:299, not d->r_e_sqr). */
 int nbx_background(void* ctx, const nbx_spots_desc* d, int out_mode, void* out, int out_on_device,
                    int64_t* first_bad);
 

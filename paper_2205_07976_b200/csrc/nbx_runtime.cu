@@ -199,6 +199,8 @@ bool trace_enabled() {
     return on;
 }
 
+constexpr double kReSqr = 7.94079248e-30;  // classical electron radius squared, m^2 (kernels.py:44)
+
 double norm3(const double* v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
 
 void check_unit(const double* v, const char* what) {
@@ -381,11 +383,18 @@ void setup_background(const nbx_spots_desc* d, nbx::SpotsParams& P, BgBufs& B) {
     P.bg_fs = static_cast<const double2*>(B.f.p);
     P.n_bg_chan = d->n_sources;
     P.bg_points = d->bg_points;
-    P.bg_scale = d->r_e_sqr * d->fluence * d->bg_thickness_factor / wsum;  // kernels.py:299
+    // kernels.py:299 uses the module constant R_E_SQR (kernels.py:44), never a context's r_e_sqr:
+    // a fused spots + background image keeps the reference's composition even when the spot
+    // context carries a non-default r_e_sqr
+    P.bg_scale = kReSqr * d->fluence * d->bg_thickness_factor / wsum;
 }
 
 // Build (or, with `reuse`, rebuild in place -- its device buffers only grow) a plan.
 constexpr int64_t kDenseMaxCells = int64_t(1) << 26;
+// Sources per launch (one plan): the channel table, runs and per-thread state of every kernel
+// variant fit the shared memory of a block at this size; longer spectra are split into
+// channel shards by nbx_spots / nbx_spots_reduce.
+constexpr int kMaxShardSources = 8192;
 
 // Sparse Fhkl table (index kind 2): open addressing, linear probing, at most half full;
 // the key packing and hash are the kernel's (nbx_kernels.cu:pack_hkl / hash_slot).  A
@@ -753,7 +762,9 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             tk.valid = true;
         }
         pt.mark("channels+upload");
-        if ((size_t)n_src * 16 > 200 * 1024) throw ArgError("too many sources in one shard (max 12800)");
+        if (n_src > kMaxShardSources)
+            throw ArgError("too many sources in one plan (max " + std::to_string(kMaxShardSources) +
+                           "; nbx_spots splits longer spectra, or shard with src_begin/src_end)");
 
         plan->bases.ensure(sizeof(double) * 9 * d->n_domains);
         NBX_CUDA(cudaMemcpy(plan->bases.p, d->bases, sizeof(double) * 9 * d->n_domains, cudaMemcpyHostToDevice));
@@ -1176,8 +1187,6 @@ void nbx_plan_destroy(void* planp) {
 int nbx_finalize(void* ctxp, const double* raw, int64_t n, double scale, int out_mode, void* out, int out_on_device,
                  int64_t* first_bad);
 
-// Sources per launch when a spectrum is too long for one kernel's shared-memory channel table.
-constexpr int kMaxShardSources = 8192;
 
 int nbx_spots(void* ctxp, const nbx_spots_desc* d, int compute, int out_mode, void* out, int out_on_device,
               int64_t* first_bad) {

@@ -159,3 +159,24 @@ def test_simulate_image_reference_signature_matches_reference_run(gpu):
             assert got.precision == "f64" and got.dims == (48, 48)
             np.testing.assert_allclose(got.data, want, rtol=2.0 ** -22, atol=0)
         assert ex.timing_log and ex.timing_log[-1].label == "simulate_image"
+
+
+def test_fused_background_ignores_context_r_e_sqr(gpu):
+    """the reference's add_background scales by the module constant R_E_SQR
+    (kernels.py:44,299) whatever the spot context's r_e_sqr; simulate_image's fused launch
+    composes f64(f32(spots with ctx.r_e_sqr)) + f64(f32(background with R_E_SQR))."""
+    import dataclasses
+
+    from paper_2205_07976_b200 import R_E_SQR
+
+    water = BackgroundProfile(points=((0.0, 2.57), (0.0365, 2.58), (0.07, 2.8), (0.12, 5.0), (0.3, 6.5)))
+    panel = synthetic.roi(synthetic.rayonix_panel(), 1880, 1880, 24, 32)
+    ctx = dataclasses.replace(synthetic.ls49_context(panel=panel, n_channels=6, n_domains=2, compute="fp64"),
+                              r_e_sqr=2.5 * R_E_SQR)
+    got = simulate_image(ctx, background=water, thickness_factor=0.7)
+    spots = PixelBuffer.zeros(panel.dims, "f32")
+    nanobragg_spots(ctx, spots)
+    bg = PixelBuffer.zeros(panel.dims, "f32")
+    add_background(water, panel, ctx.spectrum, 0.7, bg)
+    want = spots.data.astype(np.float64) + bg.data.astype(np.float64)
+    np.testing.assert_allclose(got.data, want, rtol=2.0 ** -22, atol=0)

@@ -459,6 +459,11 @@ def test_long_spectrum_is_channel_sharded_on_one_device(gpu, compute):
     got, _ = oracle_check(ctx, FP64_TOL if compute == "fp64" else FP32_TOL)
     f32 = run(ctx, "f32").data
     np.testing.assert_allclose(f32, got, rtol=2.0 ** -23, atol=0)
+    # a resident plan holds at most 8192 sources: a clear argument error, not a
+    # launch failure; its shards are fine
+    with pytest.raises(ValueError, match="max 8192"):
+        SpotsPlan(ctx)
+    SpotsPlan(ctx, src_begin=0, src_end=8192).close()
     # simulate_image / run_campaign on the long spectrum: the accumulator composed stage by
     # stage equals f64(f32(spots)) + f64(f32(background)) bit for bit, and the campaign's
     # .bin payload is that accumulator rounded to f32

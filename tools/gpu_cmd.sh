@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_multirank.py tests/test_gpu_io.py tests/test_gpu_spots.py -m gpu -q -x > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
+timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_spots.py -m gpu -q -x > gpurun_out/pytest_new.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_new.log
 tail -30 gpurun_out/pytest_new.log
