@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <mutex>
@@ -198,6 +199,16 @@ bool trace_enabled() {
     }();
     return on;
 }
+
+// NVTX ranges (the reference's kernel_timer labels, execution.py:350-356, as
+// profiler ranges): plan build, launch, download, campaign write-out.  Header-only NVTX v3:
+// no cost unless a profiler (nsys / ncu --nvtx) is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr double kReSqr = 7.94079248e-30;  // classical electron radius squared, m^2 (kernels.py:44)
 
@@ -457,6 +468,7 @@ struct PhaseTimer {
 };
 
 Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = nullptr) {
+    NvtxRange nvtx("nbx plan build");
     PhaseTimer pt;
     validate(d);
     pt.mark("validate");
@@ -901,6 +913,7 @@ void ensure_band_resources(Ctx* ctx) {
 // panel) runs on the copy stream while later bands compute, so only the last
 // band's download is exposed (the reference-facing call's end-to-end time).
 int64_t run_plan(Plan* plan, int mode, void* out, int on_device) {
+    NvtxRange nvtx(on_device ? "nbx spots (device output)" : "nbx spots (launch + download)");
     check_mode(mode);
     if (!out) throw ArgError("output buffer is NULL");
     Ctx* ctx = plan->ctx;
@@ -1409,6 +1422,7 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
         size_t bytes[2] = {0, 0};
         // render image i into slot i % 2: plan build (host), launch, then async D2H + fault read
         auto launch = [&](int i) {
+            NvtxRange nvtx("nbx campaign launch");
             const int b = i & 1;
             Plan* plan = build_plan(ctx, descs + i, compute, ctx->camp_plan[b]);
             bytes[b] = (size_t)plan->n_pixels * 4;
@@ -1495,6 +1509,7 @@ int nbx_campaign(void* ctxp, const nbx_spots_desc* descs, int n_images, int comp
                 return NBX_OK;
             }
             const auto t0 = std::chrono::steady_clock::now();
+            NvtxRange nvtx("nbx campaign crc + write");
             if (!write_image(i, ctx->camp_host[b], bytes[b])) {
                 NBX_CUDA(cudaStreamSynchronize(cs));
                 NBX_CUDA(cudaStreamSynchronize(ds));
