@@ -1,11 +1,12 @@
 """Small runs of every kernel variant, for compute-sanitizer (memcheck / racecheck / initcheck).
 
 usage: compute-sanitizer --tool memcheck python tools/sanitize_run.py
-Covers: FP32 MUFU / polynomial / degree-4 numerators, FP64 direct and recurrence, the
+Covers: FP32 MUFU / polynomial / degree-4 numerators, FP64 direct, bracket and segmented
+recurrences (incl. the direct beam's all-slow channels and span-cut runs), the
 non-grating shapes, the wide (integer) index, thickness layers + multi-panel, background
 fused into the image, the banded (pipelined) host download, add_array, noise, stats, the
 standalone background, the sparse Fhkl table, several FP64 recurrence runs, channel-shard
-partials with finalize and the slot reduction, and the pipelined campaign.
+partials with finalize and the slot reduction, and the pipelined campaign (incl. a flagged image).
 """
 import dataclasses
 import os
@@ -74,6 +75,15 @@ for compute in ("fp32", "fp64"):
 del os.environ["NBX_FHKL_HASH"]
 two_runs = synthetic.ls49_context(panel=roi, n_channels=200, n_domains=1, compute="fp64")
 run(two_runs)
+# FP64 kernel variants: the per-channel bracket recurrence and the segmented one on the direct
+# beam (S = 0: every channel slow, the limit branch), on a span-cut wide band (several runs)
+os.environ["NBX_FP64_REC"] = "1"
+run(synthetic.ls49_context(panel=roi, n_channels=64, n_domains=2, compute="fp64"))
+del os.environ["NBX_FP64_REC"]
+beam_px = synthetic.roi(synthetic.rayonix_panel(), 1915, 1915, 10, 10)
+run(synthetic.ls49_context(panel=beam_px, n_channels=32, n_domains=2, compute="fp64"), "f64")
+wide = synthetic.roi(synthetic.rayonix_panel(), 0, 0, 8, 40)
+run(synthetic.ls49_context(panel=wide, n_channels=100, de=2.0, n_domains=2, compute="fp64"))
 # channel shards: RAW partials + finalize, and the peer-memory slot reduction (one process)
 import torch  # noqa: E402
 
@@ -98,4 +108,13 @@ from paper_2205_07976_b200.io import run_campaign  # noqa: E402
 with tempfile.TemporaryDirectory() as d:
     run_campaign(lambda i: synthetic.ls49_context(synthetic.SEED + i, panel=roi, n_channels=4, n_domains=2), 3, d,
                  background=WATER)
+
+
+def hot(i):  # image 1 overflows float32: flagged, the campaign continues
+    c = synthetic.ls49_context(synthetic.SEED + i, panel=roi, n_channels=4, n_domains=2)
+    return dataclasses.replace(c, spectrum=dataclasses.replace(c.spectrum, fluence=1e64)) if i == 1 else c
+
+
+with tempfile.TemporaryDirectory() as d:
+    assert [f[0] for f in run_campaign(hot, 3, d).flagged] == [1]
 print("sanitize run complete", flush=True)
