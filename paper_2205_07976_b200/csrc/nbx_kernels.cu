@@ -830,8 +830,9 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
     const int f = blockIdx.x * kBlockX + threadIdx.x;
     const int sl = P.row0 + blockIdx.y * kBY + threadIdx.y;
     const bool inside = !(sl >= pan.slow || sl >= P.max_slow || f >= pan.fast);
-    // lanes of this warp that hold a pixel (the segmented loop's warp-uniform stops)
-    const unsigned lanes = COMPUTE == 3 ? __ballot_sync(0xFFFFFFFFu, inside) : 0u;
+    // lanes of this warp that hold a pixel (the segmented loop's warp-uniform stops and the
+    // epilogue's vectorised stores); a warp is one row of 32 consecutive fast pixels
+    const unsigned lanes = __ballot_sync(0xFFFFFFFFu, inside);
     if (!inside) return;
 
     const double b0 = P.beam[0], b1 = P.beam[1], b2 = P.beam[2];
@@ -911,17 +912,36 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
     // Fused epilogue: scale, store in the requested form, flag non-finite
     // values (kernels.py:271-273, _store_checked :211-216).
     const int64_t p = pan.out_offset + (int64_t)sl * pan.fast + f;
+    // Vectorised stores: a full warp (32 consecutive in-image pixels of one row) whose first
+    // output element is 16-byte aligned writes its row segment as 8 float4 (f32 image) or 16
+    // double2 (f64 image) from every 4th / 2nd lane, the values gathered with shuffles.
+    const int lane = threadIdx.x;
+    const bool full_warp = lanes == 0xFFFFFFFFu;
     bool bad = false;
     switch (P.out_mode) {
         case kOutF32: {
             const float v = (float)(P.out_scale * acc);
-            static_cast<float*>(P.out)[p] = v;
+            float* o = static_cast<float*>(P.out);
+            if (full_warp && (reinterpret_cast<uintptr_t>(o + (p - lane)) & 15) == 0) {
+                const float v1 = __shfl_down_sync(0xFFFFFFFFu, v, 1);
+                const float v2 = __shfl_down_sync(0xFFFFFFFFu, v, 2);
+                const float v3 = __shfl_down_sync(0xFFFFFFFFu, v, 3);
+                if ((lane & 3) == 0) *reinterpret_cast<float4*>(o + p) = make_float4(v, v1, v2, v3);
+            } else {
+                o[p] = v;
+            }
             bad = !isfinite(v);
             break;
         }
         case kOutF64: {
             const double v = P.out_scale * acc;
-            static_cast<double*>(P.out)[p] = v;
+            double* o = static_cast<double*>(P.out);
+            if (full_warp && (reinterpret_cast<uintptr_t>(o + (p - lane)) & 15) == 0) {
+                const double v1 = __shfl_down_sync(0xFFFFFFFFu, v, 1);
+                if ((lane & 1) == 0) *reinterpret_cast<double2*>(o + p) = make_double2(v, v1);
+            } else {
+                o[p] = v;
+            }
             bad = !isfinite(v);
             break;
         }

@@ -764,3 +764,29 @@ def test_caller_stream_and_probe(gpu):
         with cx.lock:
             assert cx.lib.nbx_probe_fma_peak(cx.handle, fp64, N.C.byref(tf)) == N.NBX_OK
         assert floor < tf.value < 200.0, (fp64, tf.value)
+
+
+@pytest.mark.parametrize("compute", ["fp64", "fp32"])
+def test_vectorised_stores_any_alignment(gpu, compute):
+    """The epilogue writes full 32-pixel warp rows as float4 / double2 when the row's first
+    element is 16-byte aligned and falls back to scalar stores otherwise: a device output
+    offset by 1..3 elements, odd panel widths and a partial last warp give the same pixels."""
+    import torch
+
+    from paper_2205_07976_b200 import _native as N
+
+    for rows, cols in ((6, 64), (5, 70), (3, 33)):
+        panel = synthetic.roi(synthetic.rayonix_panel(), 1880, 1880, rows, cols)
+        ctx = synthetic.ls49_context(panel=panel, n_channels=6, n_domains=2, compute=compute)
+        plan = SpotsPlan(ctx)
+        for mode, dt in ((N.OUT_F32, torch.float32), (N.OUT_F64, torch.float64)):
+            ref = None
+            for off in range(4):
+                buf = torch.zeros(plan.n_pixels + 4, dtype=dt, device="cuda")
+                plan.run(buf.data_ptr() + off * buf.element_size(), mode=mode, on_device=True)
+                img = buf[off:off + plan.n_pixels].cpu().numpy()
+                assert np.all(buf[:off].cpu().numpy() == 0) and np.all(buf[off + plan.n_pixels:].cpu().numpy() == 0)
+                if ref is None:
+                    ref = img
+                assert np.array_equal(img, ref), (rows, cols, mode, off)
+        plan.close()
