@@ -312,4 +312,21 @@ __device__ __forceinline__ AxisF32x2 axis_f32x2(f2x S, f2x D, f2x f0, f2x N, f2x
     return a;
 }
 
+// Segmented FP32 axis (variant 7): the index j is known per segment, so t = x + (-j) is one
+// packed op (exact, as the per-channel x - rint(x)); numerator on MUFU.SIN as above.
+__device__ __forceinline__ AxisF32x2 axis_seg_f32x2(f2x S, f2x D, f2x f0, f2x negj, f2x N) {
+    AxisF32x2 a;
+    const f2x x = fma2(S, D, f0);
+    const f2x t = add2(x, negj);
+    const f2x arg = mul2(N, t);  // pi N t (radians)
+    const float a0 = lo2(arg), a1 = hi2(arg);
+    const float s0 = fabsf(a0) < kSinLinear ? a0 : sin_approx_f32(a0);
+    const float s1 = fabsf(a1) < kSinLinear ? a1 : sin_approx_f32(a1);
+    a.num = pk2(s0, s1);
+    a.den = mul2(t, q_sinpi_f32x2<3>(mul2(t, t)));
+    a.j = negj;
+    a.m = x;
+    return a;
+}
+
 }  // namespace nbx

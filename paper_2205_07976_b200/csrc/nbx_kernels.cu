@@ -166,7 +166,7 @@ constexpr int kBlockY = NBX_BLOCK_Y;
 template <int COMPUTE>
 constexpr int kBlockYOf = COMPUTE == 2 ? NBX_BLOCK_Y_REC : (COMPUTE == 3 ? NBX_BLOCK_Y_SEG : NBX_BLOCK_Y);
 template <int COMPUTE>
-constexpr int kMinBlocksOf = COMPUTE == 1   ? NBX_MIN_BLOCKS_F32
+constexpr int kMinBlocksOf = COMPUTE == 1 || COMPUTE == 4 ? NBX_MIN_BLOCKS_F32
                              : COMPUTE == 2 ? NBX_MIN_BLOCKS_REC
                              : COMPUTE == 3 ? NBX_MIN_BLOCKS_SEG
                                             : NBX_MIN_BLOCKS_F64;
@@ -363,6 +363,200 @@ __device__ __forceinline__ double domain_sum_f32(const SpotsParams& P, const Chu
                                                                     c_hi, fa, fb, fc, magic_c, base, na, nb, nc);
         }
         dacc += (double)accf;
+    }
+    return dacc;
+}
+
+// ---------------------------------------------------------------------------
+// FP32 path, SEGMENTED indices (variant 7: the MUFU-numerator packed loop on uniform
+// spectra).  The packed loop above rounds every channel's phase x = S_hi D + f0 to its
+// Fhkl index j (two FMA-pipe ops per axis and channel: m = x + M, j = m - M) and gathers
+// F^2 (index ALU ops + a texture fetch) only to get t = x - j and F^2.  On a uniform
+// spectrum the phase is linear in the channel, so per chunk and axis the channel at
+// which j changes is PREDICTED (FP32: x_b + k S_hi d) and then decided EXACTLY by rounding
+// the actual x of the one or two channels within 2e-6 of the crossing (the chunk span is
+// <= 0.9, so j changes at most once per axis and chunk; tiny steps take a binary search over
+// the chunk, the rounded phase being monotone in the channel).  Every channel then gets the
+// same j as the per-channel loop, t = x - j is the same exact subtraction, and the pair
+// body is x (1 op), t (1 op), the MUFU numerator and polynomial denominator, and
+// seg += w L^2; F^2 multiplies each segment's sum once.  The two halves of a packed pair
+// are the even and odd channels: a change at channel c switches the odd half at pair c/2
+// and the even half at pair (c+1)/2, each half flushing its own segment sum.  Lanes run
+// unchecked pairs up to the warp's next event pair (__reduce_min_sync), like the FP64
+// segmented loop.  34 FMA-pipe lane-ops per channel instead of 41, no gather.
+// ---------------------------------------------------------------------------
+struct SegF32Thread {
+    float f2[3];  // F^2 (x sigma) after the 1st, 2nd, 3rd index change of the chunk
+    int c[4];     // chunk-relative channels of the changes, ascending; kSegNone-terminated
+    int ax[3];    // axis of each change, | 4 when its index steps by -1
+};
+
+constexpr int kSegNoneF32 = 0x3FFFFFFF;
+#ifndef NBX_SEG_PAIR_UNROLL
+#define NBX_SEG_PAIR_UNROLL 2
+#endif
+constexpr int kSegPairUnroll = NBX_SEG_PAIR_UNROLL;
+
+__device__ __forceinline__ float round_magic(float x) { return __fsub_rn(__fadd_rn(x, kMagicF32), kMagicF32); }
+
+__device__ __forceinline__ float chunk_D(const float4* __restrict__ sch, int p0, int k) {
+    const float4 c4 = sch[p0 + (k >> 1)];
+    return (k & 1) ? c4.y : c4.x;
+}
+
+// First chunk-relative channel whose FP32 phase fma(S, D_k, f0) rounds away from J.
+__device__ __noinline__ int f32_crossing(const float4* __restrict__ sch, int p0, int n, float S, float f0, float xb,
+                                         float J, float step) {
+    const float kstar = (J + (step > 0.0f ? 0.5f : -0.5f) - xb) / step;  // predicted crossing (>= 0)
+    if (!(kstar < (float)n)) return kSegNoneF32;                           // none (also step == 0)
+    auto is_new = [&](int k) { return round_magic(__fmaf_rn(S, chunk_D(sch, p0, k), f0)) != J; };
+    if (fabsf(step) > 4e-6f) {  // at most one channel lies within the 2e-6 prediction margin
+        const int kc = (int)ceilf(kstar);
+        if (kc >= 1 && is_new(kc - 1)) return kc - 1;
+        if (kc < n && is_new(kc)) return kc;
+        return kc + 1 < n ? kc + 1 : kSegNoneF32;
+    }
+    int lo = 0, hi = n;  // tiny steps (near the direct beam): binary search, is_new is monotone
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (is_new(mid))
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    return lo < n ? lo : kSegNoneF32;
+}
+
+template <int IDX>
+__device__ __forceinline__ double domain_sum_f32_seg(const SpotsParams& P, const ChunkF32* __restrict__ sck,
+                                                     const float4* __restrict__ sch,
+                                                     const float* __restrict__ sstep, SegF32Thread& T,
+                                                     unsigned lanes, double Sa, double Sb, double Sc) {
+    const float a_hi = __double2float_rn(Sa), b_hi = __double2float_rn(Sb), c_hi = __double2float_rn(Sc);
+    const f2x SA = bc2(a_hi), SB = bc2(b_hi), SC = bc2(c_hi);
+    const f2x Na = bc2(P.n_pi_f[0]), Nb = bc2(P.n_pi_f[1]), Nc = bc2(P.n_pi_f[2]);
+    const float* __restrict__ tab = static_cast<const float*>(P.table);
+    double dacc = 0.0;
+    for (int ci = 0; ci < P.n_chunks; ++ci) {
+        const ChunkF32 ck = sck[ci];
+        const int p0 = ck.begin, npairs = ck.end - ck.begin, n = 2 * npairs;
+        // FP64 anchor h0 = S iv0 = n0 + f0 per axis (as domain_sum_f32)
+        const double ha = Sa * ck.iv0, hb = Sb * ck.iv0, hc = Sc * ck.iv0;
+        const int na = __double2int_rn(ha), nb = __double2int_rn(hb), nc = __double2int_rn(hc);
+        const float fa = __double2float_rn(ha - (double)na);
+        const float fb = __double2float_rn(hb - (double)nb);
+        const float fc = __double2float_rn(hc - (double)nc);
+        // index of every axis at the chunk's first channel, and the (at most one) change
+        const float d0 = chunk_D(sch, p0, 0), dstep = sstep[ci];
+        const float ja = round_magic(__fmaf_rn(a_hi, d0, fa)), jb = round_magic(__fmaf_rn(b_hi, d0, fb)),
+                    jc = round_magic(__fmaf_rn(c_hi, d0, fc));
+        const float sa = a_hi * dstep, sb = b_hi * dstep, sc = c_hi * dstep;
+        int cx[3];
+        cx[0] = f32_crossing(sch, p0, n, a_hi, fa, __fmaf_rn(a_hi, d0, fa), ja, sa);
+        cx[1] = f32_crossing(sch, p0, n, b_hi, fb, __fmaf_rn(b_hi, d0, fb), jb, sb);
+        cx[2] = f32_crossing(sch, p0, n, c_hi, fc, __fmaf_rn(c_hi, d0, fc), jc, sc);
+        const int dn[3] = {sa > 0.0f ? 1 : -1, sb > 0.0f ? 1 : -1, sc > 0.0f ? 1 : -1};
+        const int ia = na + (int)ja - P.lo[0], ib = nb + (int)jb - P.lo[1], ic = nc + (int)jc - P.lo[2];
+        const float F20 = __ldg(tab + ((int64_t)ia * P.sH + (int64_t)ib * P.sK + ic));
+        {  // the changes in channel order and F^2 after each
+            int order[3] = {0, 1, 2};
+            if (cx[order[0]] > cx[order[1]]) { const int q = order[0]; order[0] = order[1]; order[1] = q; }
+            if (cx[order[1]] > cx[order[2]]) { const int q = order[1]; order[1] = order[2]; order[2] = q; }
+            if (cx[order[0]] > cx[order[1]]) { const int q = order[0]; order[0] = order[1]; order[1] = q; }
+            int da = 0, db = 0, dc = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int a = order[i];
+                T.c[i] = cx[a];
+                T.ax[i] = a | (dn[a] < 0 ? 4 : 0);
+                if (cx[a] != kSegNoneF32) {
+                    da += a == 0 ? dn[0] : 0;
+                    db += a == 1 ? dn[1] : 0;
+                    dc += a == 2 ? dn[2] : 0;
+                    T.f2[i] = __ldg(tab + ((int64_t)(ia + da) * P.sH + (int64_t)(ib + db) * P.sK + (ic + dc)));
+                }
+            }
+            T.c[3] = kSegNoneF32;
+        }
+        // per half (even / odd channels): -j per axis (packed) and F^2.  A change at channel c is
+        // handled at pair q = c / 2: the odd half switches before pair q; the even half before
+        // pair q when c is even, after it when c is odd -- one stop per change.
+        f2x NJa = bc2(-ja), NJb = bc2(-jb), NJc = bc2(-jc);
+        float F2lo = F20, F2hi = F20;
+        int ev = 0;
+        int nx = T.c[0] == kSegNoneF32 ? kSegNoneF32 : T.c[0] >> 1;
+        const f2x Fa = bc2(fa), Fb = bc2(fb), Fc = bc2(fc);
+        f2x seg = bc2(0.0f);
+        double dch = 0.0;
+        auto pair_body = [&](int q) {
+            const float4 c4 = sch[p0 + q];
+            const f2x D = pk2(c4.x, c4.y), W = pk2(c4.z, c4.w);
+            const AxisF32x2 A = axis_seg_f32x2(SA, D, Fa, NJa, Na);
+            const AxisF32x2 B = axis_seg_f32x2(SB, D, Fb, NJb, Nb);
+            const AxisF32x2 C = axis_seg_f32x2(SC, D, Fc, NJc, Nc);
+            const f2x nn = mul2(mul2(A.num, B.num), C.num);
+            const f2x dd = mul2(mul2(A.den, B.den), C.den);
+            const f2x ratio = mul2(nn, pk2(rcp_approx_f32(lo2(dd)), rcp_approx_f32(hi2(dd))));
+            seg = fma2(W, mul2(ratio, ratio), seg);
+        };
+        int q = 0;
+        for (;;) {
+            const int stop = min(__reduce_min_sync(lanes, nx), npairs);
+#pragma unroll kSegPairUnroll
+            for (; q < stop; ++q) pair_body(q);
+            if (q >= npairs) break;
+            // pair q holds index changes of some lanes (divergent, rare)
+            bool after_lo = false;  // an odd-channel change: the even half switches after pair q
+            if (nx == q) {
+                do {
+                    const int c = T.c[ev];
+                    const int a = T.ax[ev] & 3;
+                    const float d = (T.ax[ev] & 4) ? 1.0f : -1.0f;  // -j steps by -dn
+                    // the odd half: flush, switch
+                    dch = __fma_rn((double)F2hi, (double)hi2(seg), dch);
+                    seg = pk2(lo2(seg), 0.0f);
+                    if (a == 0) NJa = pk2(lo2(NJa), hi2(NJa) + d);
+                    if (a == 1) NJb = pk2(lo2(NJb), hi2(NJb) + d);
+                    if (a == 2) NJc = pk2(lo2(NJc), hi2(NJc) + d);
+                    F2hi = T.f2[ev];
+                    if ((c & 1) == 0) {  // the even half too, before the pair
+                        dch = __fma_rn((double)F2lo, (double)lo2(seg), dch);
+                        seg = pk2(0.0f, hi2(seg));
+                        if (a == 0) NJa = pk2(lo2(NJa) + d, hi2(NJa));
+                        if (a == 1) NJb = pk2(lo2(NJb) + d, hi2(NJb));
+                        if (a == 2) NJc = pk2(lo2(NJc) + d, hi2(NJc));
+                        F2lo = T.f2[ev];
+                    } else {
+                        after_lo = true;
+                    }
+                    ++ev;
+                    nx = T.c[ev] == kSegNoneF32 ? kSegNoneF32 : T.c[ev] >> 1;
+                } while (nx == q);
+            }
+            pair_body(q);
+            if (after_lo) {  // the even half takes pair q's odd changes from pair q + 1: it then holds
+                             // every change up to channel 2q + 1, exactly the odd half's state
+                dch = __fma_rn((double)F2lo, (double)lo2(seg), dch);
+                seg = pk2(0.0f, hi2(seg));
+                NJa = pk2(hi2(NJa), hi2(NJa));
+                NJb = pk2(hi2(NJb), hi2(NJb));
+                NJc = pk2(hi2(NJc), hi2(NJc));
+                F2lo = F2hi;
+            }
+            ++q;
+        }
+        dch = __fma_rn((double)F2lo, (double)lo2(seg), dch);
+        dch = __fma_rn((double)F2hi, (double)hi2(seg), dch);
+        if (isfinite(dch)) {
+            dacc += dch * kInvPi6;  // MUFU numerators carry pi N: chunk sums are pi^6 x the reference's
+        } else {  // exact Bragg position / underflow: the reference's limit branch (polynomial form)
+            const int64_t cell0 = (int64_t)(na - P.lo[0]) * P.sH + (int64_t)(nb - P.lo[1]) * P.sK + (nc - P.lo[2]);
+            const float magic_c = IDX == kIdxMagic ? kMagicF32 + (float)cell0 : kMagicF32;
+            const float* base = tab + (IDX == kIdxWide ? cell0 : -(int64_t)P.lea_bias);
+            dacc += (double)chunk_sum_f32_scalar<0, IDX, 3, true>(scalar_args(P), sch, ck.begin, ck.end, a_hi,
+                                                                   b_hi, c_hi, fa, fb, fc, magic_c, base, na, nb,
+                                                                   nc);
+        }
     }
     return dacc;
 }
@@ -796,19 +990,24 @@ __device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const
 
 // ---------------------------------------------------------------------------
 // The spot kernel.  COMPUTE: 0 = FP64 path, 1 = FP32 path, 2 = FP64 path with
-// the channel recurrence (sincg only), 3 = the segmented recurrence.
+// the channel recurrence (sincg only), 3 = the segmented recurrence, 4 = the FP32
+// MUFU loop with segmented indices.
 // ---------------------------------------------------------------------------
 template <int COMPUTE, int SHAPE, int IDX, int PDEG>
 __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMPUTE>) spots_kernel(const SpotsParams P) {
     constexpr int kBY = kBlockYOf<COMPUTE>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.y * kBlockX + threadIdx.x;
-    if constexpr (COMPUTE == 1) {
+    if constexpr (COMPUTE == 1 || COMPUTE == 4) {
         ChunkF32* k = reinterpret_cast<ChunkF32*>(smem_raw);
         for (int i = tid; i < P.n_chunks; i += kBlockX * kBY) k[i] = P.chunks[i];
         float4* s = reinterpret_cast<float4*>(smem_raw + 16 * P.n_chunks);
         const float4* g = static_cast<const float4*>(P.chan);
         for (int i = tid; i < P.n_src; i += kBlockX * kBY) s[i] = g[i];  // FP32: n_src counts pairs
+        if constexpr (COMPUTE == 4) {
+            float* st = reinterpret_cast<float*>(smem_raw + 16 * P.n_chunks + 16 * P.n_src);
+            for (int i = tid; i < P.n_chunks; i += kBlockX * kBY) st[i] = P.chunk_step[i];
+        }
     } else {
         double2* s = reinterpret_cast<double2*>(smem_raw);
         const double2* g = static_cast<const double2*>(P.chan);
@@ -879,7 +1078,15 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
                     const double Sa = r0 * __ldg(B + 0) + r1 * __ldg(B + 1) + rr2 * __ldg(B + 2);
                     const double Sb = r0 * __ldg(B + 3) + r1 * __ldg(B + 4) + rr2 * __ldg(B + 5);
                     const double Sc = r0 * __ldg(B + 6) + r1 * __ldg(B + 7) + rr2 * __ldg(B + 8);
-                    if constexpr (COMPUTE == 1) {
+                    if constexpr (COMPUTE == 4) {
+                        const size_t off = 16 * (size_t)P.n_chunks + 16 * (size_t)P.n_src;
+                        SegF32Thread* st = reinterpret_cast<SegF32Thread*>(
+                            smem_raw + ((off + 4 * (size_t)P.n_chunks + 15) & ~(size_t)15));
+                        sub += domain_sum_f32_seg<IDX>(P, reinterpret_cast<const ChunkF32*>(smem_raw),
+                                                       reinterpret_cast<const float4*>(smem_raw + 16 * P.n_chunks),
+                                                       reinterpret_cast<const float*>(smem_raw + off), st[tid],
+                                                       lanes, Sa, Sb, Sc);
+                    } else if constexpr (COMPUTE == 1) {
                         sub += domain_sum_f32<SHAPE, IDX, PDEG>(
                             P, reinterpret_cast<const ChunkF32*>(smem_raw),
                             reinterpret_cast<const float4*>(smem_raw + 16 * P.n_chunks), Sa, Sb, Sc);
@@ -1137,6 +1344,11 @@ static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape
         const size_t smem = (size_t)P.n_src * 16;
         return idx == kIdxHash ? launch_shape<0, kIdxHash>(P, shape, smem, st)
                                : launch_shape<0, kIdxWide>(P, shape, smem, st);
+    }
+    if (compute == 7) {  // FP32 MUFU-numerator loop with segmented indices (sincg, dense grid, uniform spectra)
+        const size_t off = (size_t)P.n_chunks * 16 + (size_t)P.n_src * 16 + (size_t)P.n_chunks * 4;
+        const size_t smem = ((off + 15) & ~(size_t)15) + sizeof(SegF32Thread) * kBlockX * kBlockYOf<4>;
+        return idx == kIdxWide ? launch_t<4, 0, kIdxWide, 3>(P, smem, st) : launch_t<4, 0, kIdxMagic, 3>(P, smem, st);
     }
     if (compute == 6) {  // FP64 segmented channel recurrence (sincg)
         const size_t smem = (((size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64) + 15) & ~(size_t)15) +

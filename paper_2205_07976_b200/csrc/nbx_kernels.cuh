@@ -100,6 +100,7 @@ struct SpotsParams {
     float hash_def_f;
     float pad6;
     unsigned long long table_tex;  // FP32 power-of-two table as a texture object (the packed loop's gather)
+    const float* chunk_step;       // FP32 segmented loop: each chunk's 1/lambda step (uniform spectra)
 };
 
 }  // namespace nbx

@@ -144,7 +144,8 @@ struct Plan {
     int compute = 0;
     int kernel_variant = 0;  // 0 FP64, 1 FP32 (MUFU numerator), 2 FP32 with the degree-4 polynomial
                              // (NBX_FP32_POLY=4), 5 FP32 degree 3 with the polynomial numerator,
-                             // 4 FP64 with the channel recurrence
+                             // 4 FP64 bracket recurrence, 6 FP64 segmented recurrence,
+                             // 7 FP32 MUFU numerator with segmented indices (uniform spectra)
     int shape = 0;
     bool wide = false;        // dense grid with integer index (FP32 magic window exceeded)
     bool hash = false;        // sparse Fhkl table (reachable box above kDenseMaxCells)
@@ -160,7 +161,7 @@ struct Plan {
     ~Plan() { release_tex(); }
     DevBuf hkeys, hvals;
     nbx::SpotsParams P{};
-    DevBuf panels, bases, chan, chunks, table, runs;
+    DevBuf panels, bases, chan, chunks, table, runs, chunk_step;
     HostBuf host_table;       // pinned staging of the F^2 grid
     // The device F^2 grid is rebuilt only when its inputs change: consecutive images of one
     // crystal (new orientation / mosaic / spectrum jitter) share the table, so a re-used plan
@@ -658,6 +659,17 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             // chunk is padded with a zero-weight copy of its last channel
             std::vector<nbx::ChunkF32> chunks;
             std::vector<float> ch;
+            // Segmented FP32 MUFU loop (variant 7): chunks of a uniform spectrum cut so that every
+            // reachable phase spans <= 0.9 over a chunk (at most one index change per axis), the
+            // chunk's 1/lambda step handed to the kernel for the crossing prediction.
+            // Opt-in (NBX_FP32_SEG=1): on C2 it is 116 ms against the per-channel loop's 110 ms --
+            // ~8 warp stops per 50-pair chunk cost what the 17 saved instructions per pair gain,
+            // and with 34 FMA lane-ops per channel the four MUFUs per channel co-limit.
+            const char* sev = std::getenv("NBX_FP32_SEG");
+            bool seg32 = plan->kernel_variant == 1 && d->shape == NBX_SHAPE_SINCG && !plan->hash && sev &&
+                         std::atoi(sev) == 1;
+            std::vector<float> chunk_step;
+            const double half_lim = seg32 ? 0.45 : 1.0;
             // Chunks hold <= kChunkMax channels (the FP32 partial of each packed half sums
             // <= 64 terms) and a phase-feasible run of L channels is cut into ceil(L / max)
             // chunks of equal size (C2's 100 channels: one chunk; 130: 66 + 64, not 128 + 2).
@@ -668,7 +680,7 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             while (i0 < n_src) {
                 if (i0 >= run_end) {  // next phase-feasible run and its balanced chunk size
                     run_end = i0 + 1;
-                    while (run_end < n_src && (iv[order[run_end]] - iv[order[i0]]) * 0.5 * smax <= 1.0) ++run_end;
+                    while (run_end < n_src && (iv[order[run_end]] - iv[order[i0]]) * 0.5 * smax <= half_lim) ++run_end;
                     const int len = run_end - i0, k = (len + chunk_max - 1) / chunk_max;
                     run_chunk = std::min(chunk_max, ((len + k - 1) / k + 1) / 2 * 2);  // even: whole pairs
                 }
@@ -684,7 +696,24 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
                     ++npairs;
                 }
                 chunks.push_back(nbx::ChunkF32{iv0, p0, npairs});
+                if (seg32) {  // uniform to 1e-7 of phase for every reachable S (the prediction's budget)
+                    const int len = i1 - i0;
+                    const double delta = len > 1 ? (iv[order[i1 - 1]] - iv[order[i0]]) / (double)(len - 1) : 0.0;
+                    double dev = 0.0;
+                    for (int k = 0; k < len; ++k)
+                        dev = std::max(dev, std::fabs(iv[order[i0 + k]] - iv[order[i0]] - (double)k * delta));
+                    if (dev * smax > 1e-7) seg32 = false;
+                    chunk_step.push_back((float)delta);
+                }
                 i0 = i1;
+            }
+            if (seg32 && (int64_t)chunks.size() * 8 > n_src) seg32 = false;  // chunks too short to pay off
+            if (seg32) {
+                plan->kernel_variant = 7;
+                plan->chunk_step.ensure(chunk_step.size() * sizeof(float));
+                NBX_CUDA(cudaMemcpy(plan->chunk_step.p, chunk_step.data(), chunk_step.size() * sizeof(float),
+                                    cudaMemcpyHostToDevice));
+                P.chunk_step = static_cast<const float*>(plan->chunk_step.p);
             }
             n_chan_entries = npairs;
             plan->chan.ensure(ch.size() * sizeof(float));

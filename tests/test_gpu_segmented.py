@@ -133,3 +133,30 @@ def test_two_axes_change_together(gpu, monkeypatch):
 def test_c2_takes_the_segmented_kernel(gpu):
     info = SpotsPlan(synthetic.ls49_context(compute="fp64")).info
     assert info.kernel_variant == 6 and info.channel_runs == 1
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_fp32_segmented_indices_opt_in(gpu, monkeypatch, seed):
+    """The opt-in FP32 loop with segmented indices (variant 7, NBX_FP32_SEG=1) gives the
+    per-channel loop's indices and reduced phases exactly -- only where F^2 multiplies differs
+    (1e-6) -- and matches the oracle at the FP32 tolerance, on LS49 ROIs and a wide band."""
+    from paper_2205_07976_b200 import _native as N
+
+    for r0, c0, de in ((1888, 1888, 1.0), (40, 3700, 1.0), (600, 900, 3.0)):
+        panel = synthetic.roi(synthetic.rayonix_panel(), r0, c0, 32, 48)
+        ctx = synthetic.ls49_context(synthetic.SEED + seed, panel=panel, de=de, compute="fp32")
+        imgs = {}
+        for env in ("1", "0"):
+            monkeypatch.setenv("NBX_FP32_SEG", env)
+            plan = SpotsPlan(ctx)
+            assert plan.info.kernel_variant == (7 if env == "1" else 1)
+            out = np.zeros(plan.n_pixels)
+            plan.run(out, mode=N.OUT_F64)
+            plan.close()
+            imgs[env] = out
+        monkeypatch.delenv("NBX_FP32_SEG")
+        m = parity.metrics(imgs["1"], imgs["0"], panel.dims)
+        assert m["total"] < 1e-6 and m["spot"] < 1e-6, m
+        want, _ = oracle.spots(describe(ctx), "f64")
+        m = parity.metrics(imgs["1"], want, panel.dims)
+        assert m["total"] < 1e-4 and m["spot"] < 1e-4, m
