@@ -400,6 +400,33 @@ def run_ours(args):
                         "api": "paper_2205_07976_b200.nanobragg_spots(ctx, PixelBuffer) -> nbx_spots C ABI"}
         result[f"{other}_path"] = block
 
+    if rank == 0 and not args.no_extras and world == 1 and mode == "image" and args.compute == "fp64" \
+            and _xtrace_available():
+        # the same e2e with the REFERENCE's own objects (xtrace SpotsContext / PixelBuffer from
+        # baseline/_ref) handed to the drop-in: what a reference caller patched per INTEGRATION.md gets
+        import xtrace.kernels as xk
+        import xtrace.model as xm
+
+        xs = [to_xtrace(ctx_for(3000 + i, "fp64")) for i in range(3)]
+        xtable = xs[0][0].sf_table  # one structure-factor table object for the campaign, as in the reference
+        xs = [to_xtrace(ctx_for(3000 + i, "fp64"), xtable) for i in range(3)]
+        xp = xm.DetectorPanel(panel.slow_pixels, panel.fast_pixels, panel.pixel_size, panel.distance,
+                              tuple(panel.beam_center))
+        xctx = [xk.SpotsContext(c, xp, b, oversample=1) for c, b in xs]
+        xbuf = xk.PixelBuffer.zeros(xp.dims, "f32")
+        nanobragg_spots(xctx[0], xbuf)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for c in xctx[1:]:
+            nanobragg_spots(c, xbuf)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        xms = ev0.elapsed_time(ev1) / (len(xctx) - 1)
+        result["e2e_reference_objects"] = {
+            "value": 1e3 / xms, "unit": "images/s", "ms_per_step": xms,
+            "api": "paper_2205_07976_b200.nanobragg_spots(xtrace.kernels.SpotsContext, xtrace.kernels.PixelBuffer)",
+            "note": "the reference's own input/output objects (baseline/_ref) through the drop-in, FP64"}
+
     if rank == 0 and not args.no_extras and world == 1 and mode == "image":
         result["stages"] = stage_timings(cx, N, torch, stream, ctx_for(0, args.compute), panel)
 
@@ -624,26 +651,35 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def to_xtrace(ctx, xtable=None):
+    """The reference's own objects (baseline/_ref/xtrace) for one of our SpotsContexts."""
+    import numpy as np
+    import xtrace.model as xm
+
+    c = ctx.crystal
+    if xtable is None:
+        hkl, amp = c.sf_table.arrays()
+        xtable = xm.StructureFactorTable({tuple(map(int, h)): float(a) for h, a in zip(hkl, amp)},
+                                         default_f=c.sf_table.default_f)
+    xcrystal = xm.CrystalModel(
+        cell=xm.UnitCell(c.cell.a, c.cell.b, c.cell.c, c.cell.alpha, c.cell.beta, c.cell.gamma),
+        orientation=xm.Orientation(c.orientation.u), n_cells=c.n_cells,
+        mosaic=xm.MosaicDomainSet(np.array(c.mosaic.rotations)), sf_table=xtable)
+    s = ctx.spectrum
+    xbeam = xm.BeamSpectrum(samples=s.samples, fluence=s.fluence, polarization_on=s.polarization_on,
+                            beam_direction=s.beam_direction)
+    return xcrystal, xbeam
+
+
 def _reference_step_xtrace(ctx, panel, cores):
     import multiprocessing as mp
 
-    import numpy as np
     import xtrace.kernels as xk
     import xtrace.model as xm
 
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    c = ctx.crystal
-    hkl, amp = c.sf_table.arrays()
-    xcrystal = xm.CrystalModel(
-        cell=xm.UnitCell(c.cell.a, c.cell.b, c.cell.c, c.cell.alpha, c.cell.beta, c.cell.gamma),
-        orientation=xm.Orientation(c.orientation.u), n_cells=c.n_cells,
-        mosaic=xm.MosaicDomainSet(np.array(c.mosaic.rotations)),
-        sf_table=xm.StructureFactorTable({tuple(map(int, h)): float(a) for h, a in zip(hkl, amp)},
-                                         default_f=c.sf_table.default_f))
-    s = ctx.spectrum
-    xbeam = xm.BeamSpectrum(samples=s.samples, fluence=s.fluence, polarization_on=s.polarization_on,
-                            beam_direction=s.beam_direction)
+    xcrystal, xbeam = to_xtrace(ctx)
     fork = mp.get_context("fork")
 
     def one_row(r):

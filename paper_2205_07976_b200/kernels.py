@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import math
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -142,10 +143,34 @@ def _panels_of(panel) -> tuple:
     return panel.panels if isinstance(panel, (Detector, DetectorPanel)) else (panel,)
 
 
+_XTABLE_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
 def _table_arrays(table) -> tuple[np.ndarray, np.ndarray]:
     if hasattr(table, "arrays"):
         return table.arrays()
-    # duck-typed reference StructureFactorTable (model.py:227-285): a dict of entries
+    # The reference's StructureFactorTable (model.py:227-285) keeps its entries packed and
+    # sorted for its own vectorised lookup (_packed_keys = (h+2^20)<<42 | (k+2^20)<<21 |
+    # (l+2^20), model.py:249-259): unpack those (about 1 ms for 178k entries instead of ~57 ms
+    # walking the dict) and remember the result per table object.
+    keys, vals = getattr(table, "_packed_keys", None), getattr(table, "_packed_vals", None)
+    if isinstance(keys, np.ndarray) and isinstance(vals, np.ndarray) and keys.shape == vals.shape:
+        try:
+            hit = _XTABLE_CACHE.get(table)
+        except TypeError:  # not weak-referenceable
+            hit = None
+        if hit is not None and hit[0] is keys:
+            return hit[1], hit[2]
+        b = np.int64(1 << 20)
+        k = keys.astype(np.int64)
+        hkl = np.stack([(k >> 42) - b, ((k >> 21) & 0x1FFFFF) - b, (k & 0x1FFFFF) - b], axis=1).astype(np.int32)
+        amp = np.ascontiguousarray(vals, dtype=np.float64)
+        try:
+            _XTABLE_CACHE[table] = (keys, hkl, amp)
+        except TypeError:
+            pass
+        return hkl, amp
+    # any other duck-typed table: a dict of entries
     n = len(table.entries)
     hkl = np.array(list(table.entries.keys()), dtype=np.int32).reshape(n, 3)
     amp = np.array(list(table.entries.values()), dtype=np.float64).reshape(n)
