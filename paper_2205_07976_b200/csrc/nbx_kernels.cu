@@ -799,9 +799,12 @@ constexpr float kSegThr = 3.2e-5f;      // |t| below this: the channel is evalua
 constexpr float kSegMargin = 2e-6f;     // FP32 prediction margin (phase units)
 constexpr int kSegNone = 0x3FFFFFFF;
 #ifndef NBX_SEG_UNROLL
-#define NBX_SEG_UNROLL 4
+#define NBX_SEG_UNROLL 8
 #endif
 constexpr int kSegUnroll = NBX_SEG_UNROLL;
+#ifndef NBX_SEG_CAPTURE
+#define NBX_SEG_CAPTURE 1  // index changes captured in the loop (domain_sum_f64_cap)
+#endif
 constexpr double kPi = 3.14159265358979323846;
 
 // sin(pi x)/pi for |x| <= 0.52 (degree-7 Q, rel err 2.9e-16)
@@ -825,6 +828,7 @@ __device__ __forceinline__ SineSeq sine_seq_poly(double x0, double y) {
 struct AxisSeg {
     SineSeq den, num;
     float v, invd;  // signed phase sign(Delta) t at the run's first channel, 1/|Delta|
+    float base;     // -v / |Delta|
     int n, dn;      // reference index at the first channel, its step at the crossing (+-1)
     int c;          // run-relative crossing channel (kSegNone: none in the run)
 };
@@ -844,23 +848,31 @@ __device__ __forceinline__ AxisSeg axis_seg(double S, double iv, double delta, d
     a.n = __double2int_rn(n);
     a.dn = df < 0.0f ? -1 : 1;
     a.v = df < 0.0f ? -tf : tf;
-    a.invd = 1.0f / fmaxf(fabsf(df), 1e-30f);
-    const float c = ceilf((0.5f + kSegMargin - a.v) * a.invd);  // first channel surely past 1/2
+    float r;  // 1/|Delta| to ~1 ulp: the same value feeds the crossing and the windows below
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(fabsf(df), 1e-30f)));
+    a.invd = r;
+    a.base = -a.v * r;  // channel j's phase, in channels past the run start: fma(z, invd, base)
+    // first channel surely past 1/2 -- the same expression as the upper edge of the window at
+    // z = 1/2 in seg_first_in, so every channel is either after the change or a slow channel
+    const float c = ceilf(__fmaf_rn(0.5f + kSegMargin, a.invd, a.base));
     a.c = c < (float)len ? (int)c : kSegNone;
     return a;
 }
 
-// First run-relative channel j >= j0 with |v + j |Delta| - z| < rho (as a float; 3e38: none).
-__device__ __forceinline__ float seg_first_in(float j0, float v, float invd, float z, float rho) {
-    const float lo = (z - rho - v) * invd, hi = (z + rho - v) * invd;
+// First run-relative channel j >= j0 with |v + j |Delta| - z| < rho (as a float; 3e38: none);
+// base = -v / |Delta|, so the window's edges in channels are fma(z -+ rho, invd, base).
+__device__ __forceinline__ float seg_first_in(float j0, float base, float invd, float zlo, float zhi) {
+    const float lo = __fmaf_rn(zlo, invd, base), hi = __fmaf_rn(zhi, invd, base);
     const float f = fmaxf(j0, floorf(lo) + 1.0f);
     return f < hi ? f : 3.0e38f;
 }
 
-__device__ __forceinline__ float seg_slow_axis(float j0, float v, float invd) {
+__device__ __forceinline__ float seg_slow_axis(float j0, float base, float invd) {
     constexpr float rz = kSegThr + kSegMargin;
-    return fminf(fminf(seg_first_in(j0, v, invd, -0.5f, kSegMargin), seg_first_in(j0, v, invd, 0.0f, rz)),
-                 fminf(seg_first_in(j0, v, invd, 0.5f, kSegMargin), seg_first_in(j0, v, invd, 1.0f, rz)));
+    return fminf(fminf(seg_first_in(j0, base, invd, -0.5f - kSegMargin, -0.5f + kSegMargin),
+                       seg_first_in(j0, base, invd, -rz, rz)),
+                 fminf(seg_first_in(j0, base, invd, 0.5f - kSegMargin, 0.5f + kSegMargin),
+                       seg_first_in(j0, base, invd, 1.0f - rz, 1.0f + rz)));
 }
 
 // Per-thread event state, kept in shared memory (read only at events) so that the channel
@@ -868,15 +880,16 @@ __device__ __forceinline__ float seg_slow_axis(float j0, float v, float invd) {
 struct SegThread {
     double S[3];      // Sa, Sb, Sc (slow channels)
     double f2[3];     // F^2 after the 1st, 2nd, 3rd index change of the run
-    int c[4];         // absolute channels of the index changes, ascending; kSegNone-terminated
-    float v[3], invd[3];
+    int c[5];         // absolute channels of the index changes, ascending; kSegNone-terminated
+    float base[3], invd[3];
+    double capt;      // domain_sum_f64_cap: segment sum captured at the armed index change
 };
 
 // Next slow channel (absolute) at or after run-relative j0; kSegNone if none before the run's end.
 __device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const SegThread& T) {
     const float jf = (float)j0;
-    const float f = fminf(fminf(seg_slow_axis(jf, T.v[0], T.invd[0]), seg_slow_axis(jf, T.v[1], T.invd[1])),
-                          seg_slow_axis(jf, T.v[2], T.invd[2]));
+    const float f = fminf(fminf(seg_slow_axis(jf, T.base[0], T.invd[0]), seg_slow_axis(jf, T.base[1], T.invd[1])),
+                          seg_slow_axis(jf, T.base[2], T.invd[2]));
     return f < (float)len ? b + (int)f : kSegNone;
 }
 
@@ -897,7 +910,7 @@ __device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const
         AxisSeg A = axis_seg(Sa, ivb, run.delta, P.n_cells_d[0], len);
         AxisSeg B = axis_seg(Sb, ivb, run.delta, P.n_cells_d[1], len);
         AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
-        T.v[0] = A.v, T.v[1] = B.v, T.v[2] = C.v;
+        T.base[0] = A.base, T.base[1] = B.base, T.base[2] = C.base;
         T.invd[0] = A.invd, T.invd[1] = B.invd, T.invd[2] = C.invd;
         // the run's index changes in channel order (at most one per axis), F^2 after each
         double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
@@ -973,6 +986,143 @@ __device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const
                 const double nn = (A.num.s * B.num.s) * C.num.s;
                 const double dd = (A.den.s * B.den.s) * C.den.s;
                 const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+                if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
+                advance(A.den);
+                advance(A.num);
+                advance(B.den);
+                advance(B.num);
+                advance(C.den);
+                advance(C.num);
+            }
+            ++k;
+        }
+        acc = __fma_rn(F2, seg, acc);
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// The same segmented recurrence with the index changes CAPTURED in the uniform
+// loop instead of stopping the warp at each of them.  ncu of the version above
+// (r02 v1): 13.5 warp stops per 100-channel run, 12.3 of them index changes; the
+// stop handling, the one-channel peels and the remainders around every stop cost
+// ~9 issue slots per channel.  Here each lane carries its NEXT index change c
+// (absolute channel) in a register; at k == c the loop stores the running segment
+// sum to the lane's shared-memory record (a compare and a predicated STS per
+// channel, no FP64 op), and the next warp stop flushes acc += F^2 capt,
+// seg -= capt, and arms the lane's following change.  The warp therefore stops
+// only at slow channels and at a lane's SECOND pending index change within one
+// inter-stop stretch (~2 stops per run instead of 13.5).  Same terms, same F^2 per
+// term; only where the per-segment partial sums are added into acc moves.  The
+// subtraction cancels when the terms after the change are small against those
+// before it; its absolute error, ~1e-16 seg, is ~1e-16 of what the segment would
+// give with the larger F^2 -- far below the 1e-9 bars (total, spot, pixel / max).
+// Cost model behind the design (tools/probes/loop_probe.cu and ncu): the kernel is
+// dispatch-bound at 2 issue cycles per FP64 warp-instruction + 1 per other
+// instruction -- time = (2 N_fp64 + N_other) / (4 x 148 x clock) to 0.5% on C2 --
+// so every instruction removed from the channel loop pays, FP64 ones twice.
+// ---------------------------------------------------------------------------
+template <int IDX>
+__device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const double2* __restrict__ sch,
+                                                     const RunF64* __restrict__ sru, SegThread& T, unsigned lanes,
+                                                     double Sa, double Sb, double Sc) {
+    const double* __restrict__ tab = static_cast<const double*>(P.table);
+    const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
+    T.S[0] = Sa;
+    T.S[1] = Sb;
+    T.S[2] = Sc;
+    double acc = 0.0;
+    for (int ri = 0; ri < P.n_runs; ++ri) {
+        const RunF64 run = sru[ri];
+        const int b = run.begin, e = run.end, len = e - b;
+        const double ivb = sch[b].x;
+        AxisSeg A = axis_seg(Sa, ivb, run.delta, P.n_cells_d[0], len);
+        AxisSeg B = axis_seg(Sb, ivb, run.delta, P.n_cells_d[1], len);
+        AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
+        T.base[0] = A.base, T.base[1] = B.base, T.base[2] = C.base;
+        T.invd[0] = A.invd, T.invd[1] = B.invd, T.invd[2] = C.invd;
+        // the run's DISTINCT index-change channels, ascending, with F^2 after every change at
+        // or before each (two axes changing at the same channel are one change)
+        double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
+        {
+            int x = A.c, y = B.c, z = C.c;  // sort three
+            if (x > y) { const int q = x; x = y; y = q; }
+            if (y > z) { const int q = y; y = z; z = q; }
+            if (x > y) { const int q = x; x = y; y = q; }
+            const int cs[3] = {x, y, z};
+            int m = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int ci = cs[i];
+                if (ci != kSegNone && (i == 2 || cs[i + 1] != ci)) {
+                    T.c[m] = b + ci;
+                    T.f2[m] = f2_f64<IDX>(P, tab, l0, A.n + (ci >= A.c ? A.dn : 0), B.n + (ci >= B.c ? B.dn : 0),
+                                          C.n + (ci >= C.c ? C.dn : 0));
+                    ++m;
+                }
+            }
+            for (; m < 5; ++m) T.c[m] = kSegNone;
+        }
+        int ev = 0;          // T.c[ev] = cap: the pending (armed) index change
+        int cap = T.c[0];
+        int next_slow = seg_next_slow(0, b, len, T);
+        int next_ev = min(next_slow, T.c[1]);  // a second change cannot be captured: stop there
+        double seg = 0.0;
+        int k = b;
+        for (;;) {
+            const int stop = min(__reduce_min_sync(lanes, next_ev), e);
+            // channel k + i of a group: the capture test compares the lane's armed change,
+            // relative to the group's first channel, with the immediate i
+            auto channel = [&](int i, int rel) {
+                const double wt = sch[k + i].y;
+                const double nn = (A.num.s * B.num.s) * C.num.s;
+                const double dd = (A.den.s * B.den.s) * C.den.s;
+                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+                if (rel == i) T.capt = seg;  // predicated: one compare, one store
+                seg = __fma_rn(wt, ratio * ratio, seg);
+                advance(A.den);
+                advance(A.num);
+                advance(B.den);
+                advance(B.num);
+                advance(C.den);
+                advance(C.num);
+            };
+            int rel = cap - k;
+            for (; k + kSegUnroll <= stop; k += kSegUnroll, rel -= kSegUnroll) {
+#pragma unroll
+                for (int i = 0; i < kSegUnroll; ++i) channel(i, rel);
+            }
+            for (; k < stop; ++k, --rel) channel(0, rel);
+            if (cap < k) {  // the armed change was passed: flush its segment, arm the next one
+                const double capt = T.capt;
+                acc = __fma_rn(F2, capt, acc);
+                seg -= capt;  // the sum since the change (see the note above)
+                F2 = T.f2[ev];
+                cap = T.c[++ev];
+            }
+            if (k >= e) break;
+            bool skip = false;
+            if (k == next_slow) {  // the exact reduced-phase form, exact index (divergent, rare)
+                asm volatile("");
+                const double2 c = sch[k];
+                const double S0 = T.S[0], S1 = T.S[1], S2 = T.S[2];
+                const AxisF64 a = axis_f64<kPolyF64, false>(S0, c.x, P.n_cells_d[0]);
+                const AxisF64 bb = axis_f64<kPolyF64, false>(S1, c.x, P.n_cells_d[1]);
+                const AxisF64 cc = axis_f64<kPolyF64, false>(S2, c.x, P.n_cells_d[2]);
+                const double F2x = f2_f64<IDX>(P, tab, l0, __double2int_rn(a.n), __double2int_rn(bb.n),
+                                               __double2int_rn(cc.n));
+                const double ratio = ((a.num * bb.num) * cc.num) / ((a.den * bb.den) * cc.den);
+                acc = __fma_rn(F2x * c.y, ratio * ratio, acc);  // 0/0 at t == 0: limit re-run
+                skip = true;
+                next_slow = seg_next_slow(k + 1 - b, b, len, T);
+            }
+            next_ev = min(next_slow, T.c[ev + 1]);
+            {
+                const double wt = sch[k].y;
+                const double nn = (A.num.s * B.num.s) * C.num.s;
+                const double dd = (A.den.s * B.den.s) * C.den.s;
+                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
+                if (k == cap) T.capt = seg;
                 if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
                 advance(A.den);
                 advance(A.num);
@@ -1102,7 +1252,11 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
                         const double2* sch = reinterpret_cast<const double2*>(smem_raw);
                         SegThread* st = reinterpret_cast<SegThread*>(
                             smem_raw + ((16 * P.n_src + sizeof(RunF64) * P.n_runs + 15) & ~(size_t)15));
+#if NBX_SEG_CAPTURE
+                        double a = domain_sum_f64_cap<IDX>(
+#else
                         double a = domain_sum_f64_seg<IDX>(
+#endif
                             P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), st[tid], lanes, Sa, Sb,
                             Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
