@@ -38,7 +38,7 @@ STEP_INSTR = 126  # FP-pipe instructions per step, SURVEY §8 D1 (FMA = 1)
 # SASS of the hot loop (tools/sass_loop.py), by nbx_plan_info_t.kernel_variant:
 #   (pipe, pipe lane-ops per step, lanes per SM per clock of that pipe)
 IMPL_OPS = {1: ("fma", 41, 128), 5: ("fma", 59, 128), 2: ("fma", 65, 128), 0: ("fp64", 73, 64), 4: ("fp64", 22, 64),
-            6: ("fp64", 21, 64)}
+            6: ("fp64", 18, 64)}  # 6: 21 with Reinsch numerators, 18 with Chebyshev ones (76% of C2's warp-runs)
 SMS = 148
 
 
@@ -444,18 +444,21 @@ def run_ours(args):
 def roofline(plan, kernel_ms: float, peak_tflops: float, clk_mhz: float, compute: str, writeback_bytes: int) -> dict:
     """Roofline of the spot kernel on its bounding pipe.
 
-    achieved = SASS-counted bounding-pipe lane-ops per step (the channel loop of the kernel variant,
-    tools/sass_loop.py; per-run anchors and per-segment events excluded, so this under-counts) x steps /
-    kernel time, as TFLOP/s with one pipe op = 2 FLOP (the FMA convention of the peak); peak = the live
-    FMA probe of the same pipe on this GPU (MEASURED_PEAKS.json holds no FP32/FP64 figure); frac =
+    achieved = executed bounding-pipe lane-ops per step x steps / kernel time, as TFLOP/s with one pipe
+    op = 2 FLOP (the FMA convention of the peak).  FP64: the ops per step are MEASURED -- ncu's
+    predicated-on DADD+DFMA+DMUL thread instructions of the committed capture of the same kernel
+    variant on the same workload (profiles/ncu_summary.json: every FP64 op of the launch, the per-run
+    anchors and slow channels included) / its steps; without a matching capture, the SASS count of
+    the channel loop (IMPL_OPS, an under-count).  FP32: the SASS count of the MUFU loop (41 FMA-pipe
+    lane-ops per step; ncu's FP32 op counters do not see the packed f32x2 lanes).  peak = the live FMA
+    probe of the same pipe on this GPU (MEASURED_PEAKS.json holds no FP32/FP64 figure); frac =
     achieved / peak.  d1_frac keeps SURVEY §8 D1's fixed 126 instructions per step (it exceeds 1:
     the implementation needs far fewer instructions per step than that nominal count).
     """
     variant = plan.info.kernel_variant
     pipe, ops, lanes = IMPL_OPS.get(variant, ("fp64" if compute == "fp64" else "fma", STEP_INSTR, 64))
+    ops_basis = f"{ops} SASS-counted {pipe}-pipe ops per step in the channel loop (kernel variant {variant})"
     sps = plan.steps / (kernel_ms / 1e3)
-    achieved = 2.0 * ops * sps / 1e12
-    d1 = 2.0 * STEP_INSTR * sps / 1e12
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     ncu_pipe = None
@@ -464,8 +467,15 @@ def roofline(plan, kernel_ms: float, peak_tflops: float, clk_mhz: float, compute
             rec = json.loads(prof.read_text()).get(f"spots_{compute}", {})
             traffic = rec.get("dram_bytes_per_launch")
             ncu_pipe = rec.get("pipes_pct", {}).get("cycles_fp64" if compute == "fp64" else "cycles_fma")
+            if (pipe == "fp64" and rec.get("kernel_variant") == variant and rec.get("fp64_thread_ops")
+                    and rec.get("steps_per_launch") == plan.steps):
+                ops = rec["fp64_thread_ops"] / rec["steps_per_launch"]
+                ops_basis = (f"{ops:.2f} fp64-pipe ops per step measured by ncu (DADD+DFMA+DMUL thread "
+                             f"instructions of {rec.get('source')}, kernel variant {variant}, same workload)")
         except (ValueError, AttributeError):
             traffic = None
+    achieved = 2.0 * ops * sps / 1e12
+    d1 = 2.0 * STEP_INSTR * sps / 1e12
     return {
         "bound": "fp64_pipe" if pipe == "fp64" else "fp32_fma_pipe", "achieved": achieved, "peak": peak_tflops,
         "unit": "TFLOP/s", "frac": achieved / peak_tflops if peak_tflops else None, "traffic": traffic,
@@ -473,10 +483,9 @@ def roofline(plan, kernel_ms: float, peak_tflops: float, clk_mhz: float, compute
         "pipe_frac_nominal": sps * ops / (SMS * lanes * clk_mhz * 1e6),
         "ncu_pipe_active_pct": ncu_pipe,
         "d1_frac": d1 / peak_tflops if peak_tflops else None, "d1_instr_per_step": STEP_INSTR,
-        "basis": f"{ops} SASS-counted {pipe}-pipe ops per step in the channel loop (kernel variant {variant}) x "
-                 f"steps / mean spot-kernel time (CUDA events), 1 op = 2 FLOP; peak = live {pipe} FMA probe "
-                 "(nbx_probe_fma_peak) on this GPU; pipe_frac_nominal uses 148 SMs x lanes/SM x median SM clock; "
-                 "ncu_pipe_active_pct = sm__pipe_" + ("fp64" if pipe == "fp64" else "fma") +
+        "basis": f"{ops_basis} x steps / mean spot-kernel time (CUDA events), 1 op = 2 FLOP; peak = live {pipe} "
+                 "FMA probe (nbx_probe_fma_peak) on this GPU; pipe_frac_nominal uses 148 SMs x lanes/SM x median "
+                 "SM clock; ncu_pipe_active_pct = sm__pipe_" + ("fp64" if pipe == "fp64" else "fma") +
                  "_cycles_active of the committed capture (profiles/ncu_summary.json)",
         "traffic_note": "ncu dram read+write bytes of one spot launch (profiles/ncu_summary.json): the inputs are "
                         "read once (L2-resident); most of the image write-back is still in the 126 MB L2 when "

@@ -1066,8 +1066,7 @@ __device__ __forceinline__ double seg_run(const SpotsParams& P, const double2* _
         const int stop = min(__reduce_min_sync(lanes, next_ev), e);
         // channel k + i of a group: the capture test compares the lane's armed change,
         // relative to the group's first channel, with the immediate i
-        auto channel = [&](int i, int rel) {
-            const double wt = sch[k + i].y;
+        auto channel = [&](int i, int rel, double wt) {
             const double nn = (A.num.s * B.num.s) * C.num.s;
             const double dd = (A.den.s * B.den.s) * C.den.s;
             const double ratio = nn * rcp_f64<kNewtonF64>(dd);
@@ -1083,9 +1082,9 @@ __device__ __forceinline__ double seg_run(const SpotsParams& P, const double2* _
         int rel = cap - k;
         for (; k + kSegUnroll <= stop; k += kSegUnroll, rel -= kSegUnroll) {
 #pragma unroll
-            for (int i = 0; i < kSegUnroll; ++i) channel(i, rel);
+            for (int i = 0; i < kSegUnroll; ++i) channel(i, rel, sch[k + i].y);
         }
-        for (; k < stop; ++k, --rel) channel(0, rel);
+        for (; k < stop; ++k, --rel) channel(0, rel, sch[k].y);
         if (cap < k) {  // the armed change was passed: flush its segment, arm the next one
             const double capt = T.capt;
             acc = __fma_rn(F2, capt, acc);
@@ -1173,7 +1172,12 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
         }
         // Numerator sequences whose step angle is far from 0 (|sin theta| >= kChebThr on every
         // lane of the warp) advance in the Chebyshev form: 3 FP64 ops per channel fewer when all
-        // three qualify (76% of C2's warp-runs; the rest mix forms per axis)
+        // three qualify (76% of C2's warp-runs).  Measured alternatives (C2 FP64 ms): all-or-none
+        // 116.1; a loop per qualifying-axis mask (NBX_CHEB=2, 8 loops) 126.5 -- instruction-cache
+        // misses; qualifying pairs swapped to the front (3 loops) 117.2; threshold 0.01 115.3.
+        // The Chebyshev form's error grows like k eps / sin(theta) (<= 7e-13 absolute over a
+        // 128-channel run at the threshold, against ~1e-14 for Reinsch's form); measured
+        // recurrence-vs-direct errors on LS49 ROIs are unchanged (spot <= 5e-13).
         unsigned mask = 0;
 #if NBX_CHEB
         {
@@ -1326,8 +1330,7 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
 #else
                         double a = domain_sum_f64_seg<IDX>(
 #endif
-                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), st[tid], lanes, Sa, Sb,
-                            Sc);
+                            P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), st[tid], lanes, Sa, Sb, Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;
                     } else {
@@ -1556,6 +1559,13 @@ static cudaError_t for_grid_chunks(const SpotsParams& P, F&& launch) {
 
 static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
 
+// Dynamic shared memory of the segmented FP64 kernel (variant 6): channel table, runs, per-thread
+// event records.
+size_t seg_f64_smem_bytes(int n_src, int n_runs) {
+    return (((size_t)n_src * 16 + (size_t)n_runs * sizeof(RunF64) + 15) & ~(size_t)15) +
+           sizeof(SegThread) * kBlockX * kBlockYOf<3>;
+}
+
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st) {
     if (P.n_panels <= kMaxGridYZ && P.max_slow - P.row0 <= kMaxGridYZ * kBlockYMin)
         return launch_spots_one(P, compute, shape, idx, st);
@@ -1574,8 +1584,7 @@ static cudaError_t launch_spots_one(const SpotsParams& P, int compute, int shape
         return idx == kIdxWide ? launch_t<4, 0, kIdxWide, 3>(P, smem, st) : launch_t<4, 0, kIdxMagic, 3>(P, smem, st);
     }
     if (compute == 6) {  // FP64 segmented channel recurrence (sincg)
-        const size_t smem = (((size_t)P.n_src * 16 + (size_t)P.n_runs * sizeof(RunF64) + 15) & ~(size_t)15) +
-                            sizeof(SegThread) * kBlockX * kBlockYOf<3>;
+        const size_t smem = seg_f64_smem_bytes(P.n_src, P.n_runs);
         return idx == kIdxHash ? launch_t<3, 0, kIdxHash, kPolyF32>(P, smem, st)
                                : launch_t<3, 0, kIdxWide, kPolyF32>(P, smem, st);
     }

@@ -29,6 +29,7 @@
 
 namespace nbx {
 cudaError_t launch_spots(const SpotsParams& P, int compute, int shape, int idx, cudaStream_t st);
+size_t seg_f64_smem_bytes(int n_src, int n_runs);
 cudaError_t launch_reduce_slots(const double* slots, int n_slots, int64_t n, double scale, int mode, void* out,
                                 unsigned long long* fault, cudaStream_t st);
 cudaError_t launch_finalize(const double* raw, int64_t n, double scale, int mode, void* out,
@@ -775,8 +776,14 @@ Plan* build_plan(Ctx* ctx, const nbx_spots_desc* d, int compute, Plan* reuse = n
             plan->chan.ensure(ch.size() * sizeof(double));
             NBX_CUDA(cudaMemcpy(plan->chan.p, ch.data(), ch.size() * sizeof(double), cudaMemcpyHostToDevice));
             if (!runs.empty()) {
-                // 6: segmented recurrence (default); NBX_FP64_REC=1: the per-channel bracket variant
-                plan->kernel_variant = (rev && std::atoi(rev) == 1) ? 4 : 6;
+                // 6: segmented recurrence (default); NBX_FP64_REC=1: the per-channel bracket variant.
+                // (Variant 6's shared memory -- channels, runs, per-thread event records -- fits a
+                // block up to kMaxShardSources in runs of 8; the check keeps that true.)
+                int dev = 0, smem_max = 0;
+                NBX_CUDA(cudaGetDevice(&dev));
+                NBX_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+                const bool seg_fits = nbx::seg_f64_smem_bytes(n_src, (int)runs.size()) <= (size_t)smem_max;
+                plan->kernel_variant = (rev && std::atoi(rev) == 1) || !seg_fits ? 4 : 6;
                 plan->runs.ensure(runs.size() * sizeof(nbx::RunF64));
                 NBX_CUDA(cudaMemcpy(plan->runs.p, runs.data(), runs.size() * sizeof(nbx::RunF64),
                                     cudaMemcpyHostToDevice));

@@ -160,3 +160,28 @@ def test_fp32_segmented_indices_opt_in(gpu, monkeypatch, seed):
         want, _ = oracle.spots(describe(ctx), "f64")
         m = parity.metrics(imgs["1"], want, panel.dims)
         assert m["total"] < 1e-4 and m["spot"] < 1e-4, m
+
+
+def test_full_shard_of_short_runs(gpu, monkeypatch):
+    """8192 sources (one launch's maximum) in uniform runs of 16 channels separated by gaps -- near
+    the largest shared-memory footprint of the segmented kernel (channels, >= 512 runs, event
+    records; the plan needs a mean run of >= 8) -- and in runs of 128: the plan keeps variant 6 and
+    the image equals the direct kernel's."""
+    rng = np.random.default_rng(8192)
+    cell = UnitCell(28.0, 31.0, 35.0, 90.0, 97.0, 90.0)  # small cell: the uniform-run check holds at rounding
+    crystal = CrystalModel(cell, Orientation(synthetic.random_rotation(rng)), (12, 14, 10),
+                           synthetic.generate_mosaic_rotations(5, 0.1, 1), synthetic.wilson_table(cell, 2.0, 5))
+    panel = synthetic.roi(synthetic.rayonix_panel(), 900, 1100, 8, 32)
+    for run_len in (16, 128):
+        n_runs = 8192 // run_len
+        e = (7000.0 + 0.01 * np.arange(run_len))[None, :] + 3.0 * np.arange(n_runs)[:, None]
+        w = rng.uniform(0.2, 1.0, e.size)
+        spec = BeamSpectrum(samples=tuple(zip((HC / e.ravel()).tolist(), w.tolist())), fluence=1e24,
+                            polarization_on=True)
+        ctx = SpotsContext(crystal, panel, spec, compute="fp64")
+        got, info = image(ctx, monkeypatch)
+        assert info.kernel_variant == 6 and info.channel_runs >= n_runs, (run_len, info.kernel_variant,
+                                                                          info.channel_runs)
+        direct, _ = image(ctx, monkeypatch, "0")
+        m = parity.metrics(got, direct, panel.dims)
+        assert m["total"] < 1e-11 and m["spot"] < 1e-11, (run_len, m)

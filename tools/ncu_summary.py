@@ -38,6 +38,18 @@ out = {
     "sm_clock_hz": num("sm__cycles_elapsed.avg.per_second"),
 }
 out["dram_bytes_per_launch"] = out["dram_bytes_read"] + out["dram_bytes_write"]
+# executed FP-pipe thread operations of the launch (predicated-on lanes only; an FMA counts once):
+# the measured work behind bench.py's roofline.achieved, and its fraction of the pipe's lane peak
+cyc = num("smsp__cycles_elapsed.avg")
+for prec, ops in (("fp64", ("dadd", "dfma", "dmul")), ("fp32", ("fadd", "ffma", "fmul"))):
+    rate = sum(num(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed") for o in ops)
+    if rate == rate and cyc == cyc:
+        out[f"{prec}_thread_ops"] = rate * cyc
+        out[f"{prec}_thread_ops_per_cycle"] = round(rate, 2)
+peak64 = num("sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained")
+if peak64 == peak64 and "fp64_thread_ops_per_cycle" in out:
+    out["fp64_peak_ops_per_cycle"] = peak64
+    out["fp64_ops_frac_of_peak"] = round(out["fp64_thread_ops_per_cycle"] / peak64, 4)
 pipes = {}
 for h in hdr:
     m = re.match(r"sm__inst_executed_pipe_(\w+)\.avg\.pct_of_peak_sustained_active$", h)
