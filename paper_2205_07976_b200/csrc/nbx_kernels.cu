@@ -890,9 +890,18 @@ struct SegThread {
     int c[5];         // absolute channels of the index changes, ascending; kSegNone-terminated
     float base[3], invd[3];
     double capt;      // domain_sum_f64_cap: segment sum captured at the armed index change
+    // domain_sum_f64_cap's slow channels, per axis: the next one (absolute channel, kSegNone: none),
+    // and the axis's index state (index at the run start, its change channel and step)
+    int ns[3], n[3], cx[3], dn[3];
 };
 
 // Next slow channel (absolute) at or after run-relative j0; kSegNone if none before the run's end.
+// Per-axis form for domain_sum_f64_cap: the next slow channel of axis i at or after run-relative j0.
+__device__ __forceinline__ int seg_next_slow_axis(int i, int j0, int b, int len, const SegThread& T) {
+    const float f = seg_slow_axis((float)j0, T.base[i], T.invd[i]);
+    return f < (float)len ? b + (int)f : kSegNone;
+}
+
 __device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const SegThread& T) {
     const float jf = (float)j0;
     const float f = fminf(fminf(seg_slow_axis(jf, T.base[0], T.invd[0]), seg_slow_axis(jf, T.base[1], T.invd[1])),
@@ -1058,7 +1067,13 @@ __device__ __forceinline__ double seg_run(const SpotsParams& P, const double2* _
                                           AxisSeg& C) {
     int ev = 0;          // T.c[ev] = cap: the pending (armed) index change
     int cap = T.c[0];
-    int next_slow = seg_next_slow(0, b, len, T);
+    int next_slow;
+    {
+        const int n0 = seg_next_slow_axis(0, 0, b, len, T), n1 = seg_next_slow_axis(1, 0, b, len, T),
+                  n2 = seg_next_slow_axis(2, 0, b, len, T);
+        T.ns[0] = n0, T.ns[1] = n1, T.ns[2] = n2;
+        next_slow = min(min(n0, n1), n2);
+    }
     int next_ev = min(next_slow, T.c[1]);  // a second change cannot be captured: stop there
     double seg = 0.0;
     int k = b;
@@ -1094,19 +1109,32 @@ __device__ __forceinline__ double seg_run(const SpotsParams& P, const double2* _
         }
         if (k >= e) break;
         bool skip = false;
-        if (k == next_slow) {  // the exact reduced-phase form, exact index (divergent, rare)
-            asm volatile("");
-            const double2 c = sch[k];
-            const double S0 = T.S[0], S1 = T.S[1], S2 = T.S[2];
-            const AxisF64 a = axis_f64<kPolyF64, false>(S0, c.x, P.n_cells_d[0]);
-            const AxisF64 bb = axis_f64<kPolyF64, false>(S1, c.x, P.n_cells_d[1]);
-            const AxisF64 cc = axis_f64<kPolyF64, false>(S2, c.x, P.n_cells_d[2]);
-            const double F2x = f2_f64<IDX>(P, tab, l0, __double2int_rn(a.n), __double2int_rn(bb.n),
-                                           __double2int_rn(cc.n));
-            const double ratio = ((a.num * bb.num) * cc.num) / ((a.den * bb.den) * cc.den);
+        if (k == next_slow) {  // a slow channel (divergent, rare): the axes in a slow window take the
+            asm volatile("");  // exact reduced-phase form and the reference's index (axis_f64); the
+            const double2 c = sch[k];  // others keep their (accurate there) sequence values and
+            double nn = 1.0, dd = 1.0;  // segment index -- all three carry sin(.)/pi
+            int id[3];
+            auto axis = [&](int i, const SineSeq& sd, const SineSeq& sn) {
+                if (T.ns[i] == k) {
+                    const AxisF64 a = axis_f64<kPolyF64, false>(T.S[i], c.x, P.n_cells_d[i]);
+                    nn *= a.num;
+                    dd *= a.den;
+                    id[i] = __double2int_rn(a.n);
+                    T.ns[i] = seg_next_slow_axis(i, k + 1 - b, b, len, T);
+                } else {
+                    nn *= sn.s;
+                    dd *= sd.s;
+                    id[i] = T.n[i] + (k >= T.cx[i] ? T.dn[i] : 0);
+                }
+            };
+            axis(0, A.den, A.num);
+            axis(1, B.den, B.num);
+            axis(2, C.den, C.num);
+            const double F2x = f2_f64<IDX>(P, tab, l0, id[0], id[1], id[2]);
+            const double ratio = nn / dd;
             acc = __fma_rn(F2x * c.y, ratio * ratio, acc);  // 0/0 at t == 0: limit re-run
             skip = true;
-            next_slow = seg_next_slow(k + 1 - b, b, len, T);
+            next_slow = min(min(T.ns[0], T.ns[1]), T.ns[2]);
         }
         next_ev = min(next_slow, T.c[ev + 1]);
         {
@@ -1148,6 +1176,11 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
         AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
         T.base[0] = A.base, T.base[1] = B.base, T.base[2] = C.base;
         T.invd[0] = A.invd, T.invd[1] = B.invd, T.invd[2] = C.invd;
+        T.n[0] = A.n, T.n[1] = B.n, T.n[2] = C.n;
+        T.cx[0] = A.c == kSegNone ? kSegNone : b + A.c;
+        T.cx[1] = B.c == kSegNone ? kSegNone : b + B.c;
+        T.cx[2] = C.c == kSegNone ? kSegNone : b + C.c;
+        T.dn[0] = A.dn, T.dn[1] = B.dn, T.dn[2] = C.dn;
         // the run's DISTINCT index-change channels, ascending, with F^2 after every change at
         // or before each (two axes changing at the same channel are one change)
         double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
