@@ -802,11 +802,8 @@ constexpr int kSegNone = 0x3FFFFFFF;
 #define NBX_SEG_UNROLL 8
 #endif
 constexpr int kSegUnroll = NBX_SEG_UNROLL;
-#ifndef NBX_SEG_CAPTURE
-#define NBX_SEG_CAPTURE 1  // index changes captured in the loop (domain_sum_f64_cap)
-#endif
 #ifndef NBX_CHEB
-#define NBX_CHEB 1  // Chebyshev numerators: 0 off, 1 all three axes or none, 2 per axis
+#define NBX_CHEB 1  // Chebyshev numerators: 0 off, 1 when all three axes qualify
 #endif
 #ifndef NBX_CHEB_THR
 #define NBX_CHEB_THR 0.02
@@ -902,125 +899,12 @@ __device__ __forceinline__ int seg_next_slow_axis(int i, int j0, int b, int len,
     return f < (float)len ? b + (int)f : kSegNone;
 }
 
-__device__ __forceinline__ int seg_next_slow(int j0, int b, int len, const SegThread& T) {
-    const float jf = (float)j0;
-    const float f = fminf(fminf(seg_slow_axis(jf, T.base[0], T.invd[0]), seg_slow_axis(jf, T.base[1], T.invd[1])),
-                          seg_slow_axis(jf, T.base[2], T.invd[2]));
-    return f < (float)len ? b + (int)f : kSegNone;
-}
-
-template <int IDX>
-__device__ __forceinline__ double domain_sum_f64_seg(const SpotsParams& P, const double2* __restrict__ sch,
-                                                     const RunF64* __restrict__ sru, SegThread& T, unsigned lanes,
-                                                     double Sa, double Sb, double Sc) {
-    const double* __restrict__ tab = static_cast<const double*>(P.table);
-    const int l0 = P.lo[0] * P.sH + P.lo[1] * P.sK + P.lo[2];
-    T.S[0] = Sa;
-    T.S[1] = Sb;
-    T.S[2] = Sc;
-    double acc = 0.0;
-    for (int ri = 0; ri < P.n_runs; ++ri) {
-        const RunF64 run = sru[ri];
-        const int b = run.begin, e = run.end, len = e - b;
-        const double ivb = sch[b].x;
-        AxisSeg A = axis_seg(Sa, ivb, run.delta, P.n_cells_d[0], len);
-        AxisSeg B = axis_seg(Sb, ivb, run.delta, P.n_cells_d[1], len);
-        AxisSeg C = axis_seg(Sc, ivb, run.delta, P.n_cells_d[2], len);
-        T.base[0] = A.base, T.base[1] = B.base, T.base[2] = C.base;
-        T.invd[0] = A.invd, T.invd[1] = B.invd, T.invd[2] = C.invd;
-        // the run's index changes in channel order (at most one per axis), F^2 after each
-        double F2 = f2_f64<IDX>(P, tab, l0, A.n, B.n, C.n);
-        {
-            int x = A.c, y = B.c, z = C.c;  // sort three
-            if (x > y) { const int q = x; x = y; y = q; }
-            if (y > z) { const int q = y; y = z; z = q; }
-            if (x > y) { const int q = x; x = y; y = q; }
-            const int cs[3] = {x, y, z};
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int ci = cs[i];
-                T.c[i] = ci == kSegNone ? kSegNone : b + ci;
-                if (ci != kSegNone)
-                    T.f2[i] = f2_f64<IDX>(P, tab, l0, A.n + (ci >= A.c ? A.dn : 0), B.n + (ci >= B.c ? B.dn : 0),
-                                          C.n + (ci >= C.c ? C.dn : 0));
-            }
-            T.c[3] = kSegNone;
-        }
-        int ev = 0;  // next index change
-        int next_cross = T.c[0];
-        int next_slow = seg_next_slow(0, b, len, T);
-        int next_ev = min(next_cross, next_slow);
-        double seg = 0.0;
-        int k = b;
-        for (;;) {
-            // warp-uniform stop: the first channel at which some lane of the warp has an event
-            const int stop = min(__reduce_min_sync(lanes, next_ev), e);
-            // channels before it need no test at all
-#pragma unroll kSegUnroll
-            for (; k < stop; ++k) {
-                const double wt = sch[k].y;
-                const double nn = (A.num.s * B.num.s) * C.num.s;
-                const double dd = (A.den.s * B.den.s) * C.den.s;
-                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
-                seg = __fma_rn(wt, ratio * ratio, seg);
-                advance(A.den);
-                advance(A.num);
-                advance(B.den);
-                advance(B.num);
-                advance(C.den);
-                advance(C.num);
-            }
-            if (k >= e) break;
-            bool skip = false;
-            if (k == next_ev) {  // this lane's event (divergent, rare)
-                if (k == next_cross) {  // an axis index changes: flush, switch to the prefetched F^2
-                    acc = __fma_rn(F2, seg, acc);
-                    seg = 0.0;
-                    do {  // every change at this channel (two axes may cross together)
-                        F2 = T.f2[ev];
-                        next_cross = T.c[++ev];
-                    } while (next_cross == k);
-                }
-                if (k == next_slow) {  // the exact reduced-phase form, exact index
-                    asm volatile("");
-                    const double2 c = sch[k];
-                    const double S0 = T.S[0], S1 = T.S[1], S2 = T.S[2];
-                    const AxisF64 a = axis_f64<kPolyF64, false>(S0, c.x, P.n_cells_d[0]);
-                    const AxisF64 bb = axis_f64<kPolyF64, false>(S1, c.x, P.n_cells_d[1]);
-                    const AxisF64 cc = axis_f64<kPolyF64, false>(S2, c.x, P.n_cells_d[2]);
-                    const double F2x = f2_f64<IDX>(P, tab, l0, __double2int_rn(a.n), __double2int_rn(bb.n),
-                                                   __double2int_rn(cc.n));
-                    const double ratio = ((a.num * bb.num) * cc.num) / ((a.den * bb.den) * cc.den);
-                    acc = __fma_rn(F2x * c.y, ratio * ratio, acc);  // 0/0 at t == 0: limit re-run
-                    skip = true;
-                    next_slow = seg_next_slow(k + 1 - b, b, len, T);
-                }
-                next_ev = min(next_cross, next_slow);
-            }
-            {
-                const double wt = sch[k].y;
-                const double nn = (A.num.s * B.num.s) * C.num.s;
-                const double dd = (A.den.s * B.den.s) * C.den.s;
-                const double ratio = nn * rcp_f64<kNewtonF64>(dd);
-                if (!skip) seg = __fma_rn(wt, ratio * ratio, seg);
-                advance(A.den);
-                advance(A.num);
-                advance(B.den);
-                advance(B.num);
-                advance(C.den);
-                advance(C.num);
-            }
-            ++k;
-        }
-        acc = __fma_rn(F2, seg, acc);
-    }
-    return acc;
-}
 
 // ---------------------------------------------------------------------------
-// The same segmented recurrence with the index changes CAPTURED in the uniform
-// loop instead of stopping the warp at each of them.  ncu of the version above
-// (r02 v1): 13.5 warp stops per 100-channel run, 12.3 of them index changes; the
+// The segmented recurrence's channel loop, with the index changes CAPTURED in the
+// uniform loop instead of stopping the warp at each of them.  ncu of the first
+// version, which stopped at every event (r02 v1, in git history as
+// domain_sum_f64_seg): 13.5 warp stops per 100-channel run, 12.3 of them index changes; the
 // stop handling, the one-channel peels and the remainders around every stop cost
 // ~9 issue slots per channel.  Here each lane carries its NEXT index change c
 // (absolute channel) in a register; at k == c the loop stores the running segment
@@ -1206,7 +1090,7 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
         // Numerator sequences whose step angle is far from 0 (|sin theta| >= kChebThr on every
         // lane of the warp) advance in the Chebyshev form: 3 FP64 ops per channel fewer when all
         // three qualify (76% of C2's warp-runs).  Measured alternatives (C2 FP64 ms): all-or-none
-        // 116.1; a loop per qualifying-axis mask (NBX_CHEB=2, 8 loops) 126.5 -- instruction-cache
+        // 116.1; a loop per qualifying-axis mask (8 loops) 126.5 -- instruction-cache
         // misses; qualifying pairs swapped to the front (3 loops) 117.2; threshold 0.01 115.3.
         // The Chebyshev form's error grows like k eps / sin(theta) (<= 7e-13 absolute over a
         // 128-channel run at the threshold, against ~1e-14 for Reinsch's form); measured
@@ -1219,9 +1103,7 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
                          sc = C.num.a * (1.0 - 0.25 * C.num.a);  // sin^2(theta) = alpha (1 - alpha / 4)
             mask = (__all_sync(lanes, sa >= thr2) ? 1u : 0u) | (__all_sync(lanes, sb >= thr2) ? 2u : 0u) |
                    (__all_sync(lanes, sc >= thr2) ? 4u : 0u);
-#if NBX_CHEB == 1
             mask = mask == 7u ? 7u : 0u;
-#endif
             if (mask & 1u) to_cheb(A.num);
             if (mask & 2u) to_cheb(B.num);
             if (mask & 4u) to_cheb(C.num);
@@ -1231,9 +1113,6 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
 #define NBX_SEG_CASE(M) \
     case M: acc = seg_run<IDX, M>(P, sch, tab, T, lanes, l0, b, e, len, F2, acc, A, B, C); break;
             NBX_SEG_CASE(0)
-#if NBX_CHEB == 2
-            NBX_SEG_CASE(1) NBX_SEG_CASE(2) NBX_SEG_CASE(3) NBX_SEG_CASE(4) NBX_SEG_CASE(5) NBX_SEG_CASE(6)
-#endif
 #if NBX_CHEB
             NBX_SEG_CASE(7)
 #endif
@@ -1358,11 +1237,7 @@ __global__ void __launch_bounds__(kBlockX* kBlockYOf<COMPUTE>, kMinBlocksOf<COMP
                         const double2* sch = reinterpret_cast<const double2*>(smem_raw);
                         SegThread* st = reinterpret_cast<SegThread*>(
                             smem_raw + ((16 * P.n_src + sizeof(RunF64) * P.n_runs + 15) & ~(size_t)15));
-#if NBX_SEG_CAPTURE
                         double a = domain_sum_f64_cap<IDX>(
-#else
-                        double a = domain_sum_f64_seg<IDX>(
-#endif
                             P, sch, reinterpret_cast<const RunF64*>(smem_raw + 16 * P.n_src), st[tid], lanes, Sa, Sb, Sc);
                         if (!isfinite(a)) a = channel_sum_f64<0, true, IDX>(P, sch, Sa, Sb, Sc);  // limit branch
                         sub += a;

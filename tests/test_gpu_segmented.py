@@ -1,4 +1,4 @@
-"""The segmented FP64 channel recurrence (kernel variant 6, nbx_kernels.cu:domain_sum_f64_seg).
+"""The segmented FP64 channel recurrence (kernel variant 6, nbx_kernels.cu:domain_sum_f64_cap).
 
 Per run the kernel predicts, in FP32, the channel at which each axis's Fhkl index changes and
 the channels that sit within the margins of a half-integer (index not provable) or within
