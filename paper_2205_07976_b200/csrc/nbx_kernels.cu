@@ -1091,7 +1091,8 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
         // lane of the warp) advance in the Chebyshev form: 3 FP64 ops per channel fewer when all
         // three qualify (76% of C2's warp-runs).  Measured alternatives (C2 FP64 ms): all-or-none
         // 116.1; a loop per qualifying-axis mask (8 loops) 126.5 -- instruction-cache
-        // misses; qualifying pairs swapped to the front (3 loops) 117.2; threshold 0.01 115.3.
+        // misses; qualifying pairs swapped to the front (3 loops) 117.2 and, with the per-axis slow
+        // channels, 123.4 vs 115.9 (spills, three loop bodies); threshold 0.01 115.3.
         // The Chebyshev form's error grows like k eps / sin(theta) (<= 7e-13 absolute over a
         // 128-channel run at the threshold, against ~1e-14 for Reinsch's form); measured
         // recurrence-vs-direct errors on LS49 ROIs are unchanged (spot <= 5e-13).
