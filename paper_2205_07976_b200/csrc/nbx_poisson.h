@@ -12,10 +12,15 @@
 //     libdevice differ in the last ulp).
 //   * Sampler: inversion (sequential search) for mean < 12, Hormann's PTRS
 //     transformed rejection (1993) above.
+//   * Cheap and divergence-light (a warp's lanes take different branches): log(k!) and
+//     1/k from tables of correctly rounded constants, powers of two and frexp from the
+//     double's bits (exact, so identical to ldexp / frexp), no per-step division in the
+//     inversion search.
 #pragma once
 
 #include <stdint.h>
 #include <math.h>
+#include <string.h>
 
 #if defined(__CUDACC__)
 #define NBX_HD __host__ __device__ __forceinline__
@@ -34,6 +39,126 @@
 #endif
 
 namespace nbx {
+
+// Bit views of a double (exact, both builds).
+NBX_HD uint64_t det_bits(double x) {
+#if defined(__CUDA_ARCH__)
+    return (uint64_t)__double_as_longlong(x);
+#else
+    uint64_t u;
+    memcpy(&u, &x, sizeof u);
+    return u;
+#endif
+}
+NBX_HD double det_from_bits(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)u);
+#else
+    double x;
+    memcpy(&x, &u, sizeof x);
+    return x;
+#endif
+}
+
+// x 2^k, k integral: one exact-product rounding, identical to ldexp; 2^k is built from its bits
+// while it is a normal number (k >= -1022), ldexp below.
+NBX_HD double det_scale2(double x, int k) {
+    if (k >= -1022 && k <= 1023) return NBX_MUL(x, det_from_bits((uint64_t)(k + 1023) << 52));
+    return ldexp(x, k);
+}
+
+// log(k!) for k < 16, correctly rounded (decimal, 50 digits)
+#if defined(__CUDA_ARCH__)
+__device__
+#endif
+static const double kDetLogFact[16] = {
+    0.0,
+    0.0,
+    0.6931471805599453,
+    1.791759469228055,
+    3.1780538303479458,
+    4.787491742782046,
+    6.579251212010101,
+    8.525161361065415,
+    10.60460290274525,
+    12.801827480081469,
+    15.104412573075516,
+    17.502307845873887,
+    19.987214495661885,
+    22.552163853123425,
+    25.19122118273868,
+    27.89927138384089};
+
+// 1/k for k <= 64, correctly rounded (IEEE division)
+#if defined(__CUDA_ARCH__)
+__device__
+#endif
+static const double kDetInv[65] = {
+    0.0,
+    1.0,
+    0.5,
+    0.3333333333333333,
+    0.25,
+    0.2,
+    0.16666666666666666,
+    0.14285714285714285,
+    0.125,
+    0.1111111111111111,
+    0.1,
+    0.09090909090909091,
+    0.08333333333333333,
+    0.07692307692307693,
+    0.07142857142857142,
+    0.06666666666666667,
+    0.0625,
+    0.058823529411764705,
+    0.05555555555555555,
+    0.05263157894736842,
+    0.05,
+    0.047619047619047616,
+    0.045454545454545456,
+    0.043478260869565216,
+    0.041666666666666664,
+    0.04,
+    0.038461538461538464,
+    0.037037037037037035,
+    0.03571428571428571,
+    0.034482758620689655,
+    0.03333333333333333,
+    0.03225806451612903,
+    0.03125,
+    0.030303030303030304,
+    0.029411764705882353,
+    0.02857142857142857,
+    0.027777777777777776,
+    0.02702702702702703,
+    0.02631578947368421,
+    0.02564102564102564,
+    0.025,
+    0.024390243902439025,
+    0.023809523809523808,
+    0.023255813953488372,
+    0.022727272727272728,
+    0.022222222222222223,
+    0.021739130434782608,
+    0.02127659574468085,
+    0.020833333333333332,
+    0.02040816326530612,
+    0.02,
+    0.0196078431372549,
+    0.019230769230769232,
+    0.018867924528301886,
+    0.018518518518518517,
+    0.01818181818181818,
+    0.017857142857142856,
+    0.017543859649122806,
+    0.017241379310344827,
+    0.01694915254237288,
+    0.016666666666666666,
+    0.01639344262295082,
+    0.016129032258064516,
+    0.015873015873015872,
+    0.015625};
 
 struct Philox4 {
     uint32_t v[4];
@@ -70,7 +195,7 @@ NBX_HD Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
 // 53-bit uniform in the open interval (0, 1) from two 32-bit words.
 NBX_HD double u53(uint32_t a, uint32_t b) {
     const uint64_t m = ((uint64_t)(a >> 5) << 26) | (uint64_t)(b >> 6);  // 27 + 26 bits
-    return NBX_ADD(ldexp((double)m, -53), ldexp(1.0, -54));
+    return NBX_ADD(NBX_MUL((double)m, 0x1p-53), 0x1p-54);  // exact scalings
 }
 
 // exp(x) for x in [-745, 0]: Cody-Waite reduction by ln 2 and a degree-11 Taylor
@@ -94,13 +219,21 @@ NBX_HD double det_exp(double x) {
     p = NBX_ADD(NBX_MUL(p, r), 0.5);
     p = NBX_ADD(NBX_MUL(p, r), 1.0);
     p = NBX_ADD(NBX_MUL(p, r), 1.0);
-    return ldexp(p, (int)kf);
+    return det_scale2(p, (int)kf);
 }
 
 // log(x) for finite x > 0: x = m 2^e, m in [sqrt(1/2), sqrt(2)), atanh series.
 NBX_HD double det_log(double x) {
     int e;
-    double m = frexp(x, &e);  // m in [0.5, 1)
+    double m;
+    const uint64_t bits = det_bits(x);
+    const int ef = (int)((bits >> 52) & 0x7FF);
+    if (ef != 0) {  // normal: frexp from the bits (m in [0.5, 1))
+        e = ef - 1022;
+        m = det_from_bits((bits & 0x800FFFFFFFFFFFFFull) | (1022ull << 52));
+    } else {
+        m = frexp(x, &e);  // subnormal
+    }
     if (m < 0.70710678118654752440) {
         m = NBX_MUL(m, 2.0);
         e -= 1;
@@ -125,11 +258,7 @@ NBX_HD double det_log(double x) {
 
 // log(k!) : exact-table for k < 16, Stirling series above.
 NBX_HD double det_log_factorial(double k) {
-    if (k < 16.0) {
-        double acc = 0.0;
-        for (int i = 2; i <= (int)k; ++i) acc = NBX_ADD(acc, det_log((double)i));
-        return acc;
-    }
+    if (k < 16.0) return kDetLogFact[(int)k];
     const double x = NBX_ADD(k, 1.0);
     const double ix = 1.0 / x;
     const double ix2 = NBX_MUL(ix, ix);
@@ -159,7 +288,8 @@ NBX_HD double poisson_draw(double mu, uint64_t seed, uint64_t image, uint64_t pi
         double k = 0.0;
         while (u > F && k < 1000.0) {
             k = NBX_ADD(k, 1.0);
-            p = NBX_MUL(p, mu / k);
+            const double inv_k = k <= 64.0 ? kDetInv[(int)k] : 1.0 / k;
+            p = NBX_MUL(p, NBX_MUL(mu, inv_k));
             F = NBX_ADD(F, p);
         }
         return k;
