@@ -809,6 +809,7 @@ constexpr int kSegUnroll = NBX_SEG_UNROLL;
 #define NBX_CHEB_THR 0.02
 #endif
 constexpr double kChebThr = NBX_CHEB_THR;  // |sin(theta)| of a numerator step below which Reinsch's form stays
+constexpr double kChebNear = 0.0055;  // eps / (2 pi kSegThr 2e-10), eps = 2.2e-16: see domain_sum_f64_cap
 constexpr double kPi = 3.14159265358979323846;
 
 // sin(pi x)/pi for |x| <= 0.52 (degree-7 Q, rel err 2.9e-16)
@@ -1099,11 +1100,18 @@ __device__ __forceinline__ double domain_sum_f64_cap(const SpotsParams& P, const
         unsigned mask = 0;
 #if NBX_CHEB
         {
-            const double thr2 = kChebThr * kChebThr;
+            // per axis: |sin theta| >= max(kChebThr, len kChebNear / N) -- the second term keeps the
+            // form's drift (<= len eps / (2 sin theta)) below 2e-10 of a numerator next to a slow
+            // window (|sin(pi N t)| ~ pi N kSegThr), for small N or long runs
+            auto thr2 = [&](double N) {  // FP32 is plenty for a threshold
+                const float t = fmaxf((float)kChebThr, (float)len * (float)kChebNear * rcp_approx_f32((float)N));
+                return (double)(t * t);
+            };
             const double sa = A.num.a * (1.0 - 0.25 * A.num.a), sb = B.num.a * (1.0 - 0.25 * B.num.a),
                          sc = C.num.a * (1.0 - 0.25 * C.num.a);  // sin^2(theta) = alpha (1 - alpha / 4)
-            mask = (__all_sync(lanes, sa >= thr2) ? 1u : 0u) | (__all_sync(lanes, sb >= thr2) ? 2u : 0u) |
-                   (__all_sync(lanes, sc >= thr2) ? 4u : 0u);
+            mask = (__all_sync(lanes, sa >= thr2(P.n_cells_d[0])) ? 1u : 0u) |
+                   (__all_sync(lanes, sb >= thr2(P.n_cells_d[1])) ? 2u : 0u) |
+                   (__all_sync(lanes, sc >= thr2(P.n_cells_d[2])) ? 4u : 0u);
             mask = mask == 7u ? 7u : 0u;
             if (mask & 1u) to_cheb(A.num);
             if (mask & 2u) to_cheb(B.num);
