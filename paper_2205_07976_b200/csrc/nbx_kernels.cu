@@ -15,8 +15,11 @@
 //     throughput kernel), 5 = same loop with the polynomial numerator (few samples
 //     per pixel), 4 = degree-4 polynomials; non-grating shapes and the wide / hash
 //     Fhkl indices take the scalar loop.
+//   COMPUTE 4 FP32 path, packed loop with segmented indices (opt-in, NBX_FP32_SEG=1).
 //   COMPUTE 0 FP64 path, direct per-channel evaluation; COMPUTE 2 FP64 path with the
-//     channel recurrence (uniform 1/lambda runs).
+//     per-channel bracket recurrence (NBX_FP64_REC=1); COMPUTE 3 FP64 path with the
+//     segmented recurrence (uniform 1/lambda runs; the FP64 default, plan variant 6:
+//     domain_sum_f64_cap) on 32x4 blocks.
 //   IDX: Fhkl index kind -- magic-float bit patterns on a power-of-two grid, integer
 //     index on a dense grid, or the sparse hash table.
 #include <cuda_runtime.h>
