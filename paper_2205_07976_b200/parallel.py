@@ -235,6 +235,15 @@ def simulate_channel_sharded(ctx: SpotsContext, out: PixelBuffer | None = None, 
         return _p2p_channel_sharded(ctx, out, group, root, world, rank)
     if transport == "native":
         return _native_channel_sharded(ctx, out, group, root, rank)
+    if world == 1 and partial is None and finalize is None:
+        # one shard is the whole spectrum: the single-image call (same arithmetic -- unscaled
+        # FP64 sum, one scale, one cast -- with the row-banded download overlapping the kernel)
+        from .kernels import nanobragg_spots
+
+        if out is None:
+            out = PixelBuffer.zeros(ctx.panel.dims, "f32")
+        nanobragg_spots(ctx, out)
+        return out
     partial = partial or _gpu_partial
     finalize = finalize or _gpu_finalize
     lo, hi = channel_shards(n_src, world)[rank]

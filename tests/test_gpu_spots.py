@@ -536,11 +536,16 @@ def test_channel_sharded_path_single_rank(gpu, compute):
     ctx = roi_ctx(compute)
     rtol = 1e-13 if compute == "fp64" else 2e-6
     direct = run(ctx, "f64").data
-    got = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(ctx.panel.dims, "f64"))
+    # the partial -> finalize pieces themselves (a single rank's default call skips them: one
+    # shard is the whole spectrum, so it takes the single-image call with the banded download)
+    pieces = dict(partial=parallel._gpu_partial, finalize=parallel._gpu_finalize)
+    got = parallel.simulate_channel_sharded(ctx, PixelBuffer.zeros(ctx.panel.dims, "f64"), **pieces)
     np.testing.assert_allclose(got.data, direct, rtol=rtol, atol=0)
-    f32 = parallel.simulate_channel_sharded(ctx)
+    f32 = parallel.simulate_channel_sharded(ctx, **pieces)
     assert f32.precision == "f32"
     np.testing.assert_allclose(f32.data, direct.astype(np.float32), rtol=max(rtol, 2e-7))
+    default = parallel.simulate_channel_sharded(ctx)  # single rank: the single-image call
+    assert default.precision == "f32" and np.array_equal(default.data, run(ctx, "f32").data)
 
 
 def test_nanobragg_facade_matches_api(gpu):
